@@ -1,0 +1,170 @@
+/*
+ * hb.h -- C ABI of the B200-native rank-reveal path (seeded cube-pair kernel assembly + ε-rank).
+ *
+ * The reference (/root/reference/proj/include/hodlr/) is a header-only C++20 library whose
+ * interface for this path is value types + free functions with C++ exceptions.  This header is
+ * the drop-in boundary a binding would target (see INTEGRATION.md for the C++ / ctypes stubs):
+ * plain C structs, pointers and sizes, status codes instead of exceptions, no torch or CUDA
+ * types in any signature (streams are passed as void*).
+ *
+ * Reference interface each entry point replaces:
+ *   hb_kernel              <- hodlr::KernelSpec / KernelId          kernel.hpp:19-32, 37-110
+ *   hb_cube                <- hodlr::HyperCube{lower, side}         geometry.hpp:15-64
+ *   hb_pair.d_prime        <- hodlr::InteractionClass (far / surface:d')  geometry.hpp:77-104
+ *   hb_generate_points     <- SPEC pair_geometry (X, Y point sets)
+ *   hb_assemble            <- hodlr::assemble_dense                 kernel.hpp:168-181
+ *   hb_eval_radial_host    <- hodlr::eval_radial (scalar, host)     kernel.hpp:149-157
+ *   hb_rank_matrix         <- SPEC epsilon_rank(matrix, epsilon)
+ *   hb_rank                <- SPEC pair_geometry -> assemble_dense -> epsilon_rank
+ *   hb_sweep               <- SPEC rank_table + parallel_for        SPEC.md:570-578, parallel.hpp:12-29
+ * Error mapping (reference exceptions -> status):
+ *   std::invalid_argument -> HB_EINVAL   (kernel.hpp:171-173, geometry.hpp:22)
+ *   std::length_error     -> HB_ECAP     (kernel.hpp:174-175, entry cap)
+ *   std::domain_error / non-finite entries -> HB_EDOMAIN
+ *   std::runtime_error r == 0 on a singular kernel without diagonal -> HB_ESINGULAR (kernel.hpp:152-153)
+ *   KernelId::Custom (std::function, cannot cross to the device), J2/Y2 -> HB_EUNSUPPORTED
+ * No C++ exception ever crosses this ABI.
+ *
+ * Rank semantics: rank = count of singular values σ_k > tol·σ₁.
+ * The device factorisation is a sketch-pivoted blocked Householder QR stopped once the
+ * residual ‖A22‖_F ≤ η·tol·σ₁; the rank is then certified from the singular values of the
+ * leading k rows of R:  rank_lo = #σ(R_k) > thr  ≤  true rank  ≤  rank_hi = #σ(R_k) > sqrt(thr² − δ²).
+ */
+#ifndef HB_H
+#define HB_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  HB_OK = 0,
+  HB_EINVAL = 1,
+  HB_EDOMAIN = 2,
+  HB_ECAP = 3,
+  HB_ESINGULAR = 4,
+  HB_EUNSUPPORTED = 5,
+  HB_ENOMEM = 6,
+  HB_ECUDA = 7,
+  HB_ENCCL = 8
+} hb_status;
+
+/* KernelId order of kernel.hpp:19-32. */
+enum {
+  HB_K_INVERSE_R = 0, HB_K_LOG_R = 1, HB_K_HELMHOLTZ3D_RE = 2, HB_K_HELMHOLTZ3D_IM = 3,
+  HB_K_HANKEL_H12_RE = 4, HB_K_HANKEL_H12_IM = 5, HB_K_R = 6, HB_K_SIN_R = 7,
+  HB_K_INV_SQRT_1_PLUS_R = 8, HB_K_EXP_NEG_R = 9, HB_K_EXP_NEG_R2 = 10, HB_K_CUSTOM = 11
+};
+
+/* Point modes. */
+enum { HB_POINTS_UNIFORM = 0, HB_POINTS_GRID_INTERIOR = 1, HB_POINTS_GRID_CLOSED = 2 };
+
+/* KernelSpec: id + optional diagonal value used when r == 0 (kernel.hpp:37-61). */
+typedef struct {
+  int32_t id;
+  int32_t has_diag;
+  double diag;
+} hb_kernel;
+
+/* HyperCube: lower corner (d <= 8 coordinates) and side (> 0). */
+typedef struct {
+  int32_t d;
+  int32_t reserved;
+  double lower[8];
+  double side;
+} hb_cube;
+
+/* A target/source cube pair with its point clouds.
+ * d_prime: -1 far-field, else dimension of the shared hyper-surface (descriptor only; the
+ * geometry itself is carried by the cubes). */
+typedef struct {
+  hb_cube target;
+  hb_cube source;
+  int32_t d_prime;
+  int32_t point_mode;
+  int64_t n_target;
+  int64_t n_source;
+  uint64_t seed;
+} hb_pair;
+
+/* One rank result per tolerance. */
+typedef struct {
+  int32_t rank;        /* = rank_lo: #σ(R_k) > tol·σ₁ */
+  int32_t rank_lo;
+  int32_t rank_hi;     /* #σ(R_k) > sqrt(thr² − δ²); == rank_lo when certified */
+  int32_t k_factored;  /* columns of the pivoted QR kept before certification */
+  double sigma1;
+  double sigma_r;      /* σ_p   (0 if p == 0) */
+  double sigma_r1;     /* σ_{p+1} (0 if p == min(m, n)) */
+  double gap;          /* min(σ_p/thr − 1, 1 − σ_{p+1}/thr) */
+  double resid;        /* δ = ‖A22‖_F after k_factored columns */
+  double sec[4];       /* device seconds: points+assembly, factorisation, certification, total */
+} hb_rank_result;
+
+#define HB_MAX_TOLS 4
+/* One sweep entry: kernel x pair x up to four tolerances. */
+typedef struct {
+  hb_kernel kernel;
+  hb_pair pair;
+  double tols[HB_MAX_TOLS];
+  int32_t ntol;
+  int32_t reserved;
+} hb_problem;
+
+typedef struct hb_context hb_context; /* opaque; one per device and host thread */
+
+const char* hb_version(void);
+const char* hb_status_string(hb_status s);
+/* Last error detail recorded on this context (or the global one if ctx == NULL). */
+const char* hb_last_error(const hb_context* ctx);
+
+hb_status hb_context_create(int device, hb_context** out);
+void hb_context_destroy(hb_context* ctx);
+/* The CUDA stream (cudaStream_t) all work of this context is ordered on. */
+void* hb_context_stream(hb_context* ctx);
+/* Tuning: block size cap (8..120, multiple of 8) and stop factor η (0 < η <= 0.1). */
+hb_status hb_context_set_tuning(hb_context* ctx, int32_t block_max, double eta);
+
+/* k1: seeded / grid points, SoA (coordinate k of point i at k*n + i), device pointers. */
+hb_status hb_generate_points(hb_context* ctx, const hb_pair* pair, double* d_tgt_soa,
+                             double* d_src_soa);
+
+/* k2: K(i,j) = F(||x_i - y_j||_2), column-major T x N, leading dimension ldk >= T.
+ * Device pointers; ordered on the context stream; synchronises to report ESINGULAR/EDOMAIN. */
+hb_status hb_assemble(hb_context* ctx, const hb_kernel* kernel, const double* d_tgt_soa, int64_t T,
+                      const double* d_src_soa, int64_t N, int32_t d, double* d_K, int64_t ldk);
+
+/* Scalar host evaluation of F(r) with the r == 0 rule (kernel.hpp:149-157). */
+hb_status hb_eval_radial_host(const hb_kernel* kernel, double r, double* out);
+
+/* ε-rank of a caller-provided device matrix (column-major m x n, leading dimension ld).
+ * The matrix is copied into context workspace; the input is not modified. */
+hb_status hb_rank_matrix(hb_context* ctx, const double* d_A, int64_t m, int64_t n, int64_t ld,
+                         const double* tols, int32_t ntol, hb_rank_result* out);
+
+/* k1 + k2 + k3: generate, assemble and rank one pair (out has ntol entries). */
+hb_status hb_rank(hb_context* ctx, const hb_kernel* kernel, const hb_pair* pair,
+                  const double* tols, int32_t ntol, hb_rank_result* out);
+
+/* Singular values (descending) of R_k from the last certification on this context.
+ * Copies min(max, count) values to host_out; *count = number available. */
+hb_status hb_last_sigma(hb_context* ctx, double* host_out, int64_t max, int64_t* count);
+
+/* k4: run n independent problems over ndev devices (LPT partition on a cost model, one worker
+ * thread per device).  out: sum of ntol over problems, problem-major.  Per-problem status codes
+ * go to status_out (may be NULL); the return value is the first failure or HB_OK. */
+hb_status hb_sweep(const hb_problem* probs, int64_t n, const int32_t* devices, int32_t ndev,
+                   hb_rank_result* out, int32_t* status_out);
+
+/* LPT assignment used by hb_sweep / multi-process sweeps: owner[i] in [0, nparts). */
+hb_status hb_partition(const hb_problem* probs, int64_t n, int32_t nparts, int32_t* owner);
+
+/* Deterministic per-problem seed = hash(base, d, d', N). */
+uint64_t hb_problem_seed(uint64_t base, int32_t d, int32_t d_prime, int64_t n);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

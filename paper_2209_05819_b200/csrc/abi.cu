@@ -1,0 +1,437 @@
+// C ABI (include/hb.h): argument validation mirroring the reference's exceptions, k1/k2 entry
+// points, hb_rank / hb_rank_matrix, the multi-device sweep driver (k4) and its LPT partition.
+// No C++ exception crosses this file's extern "C" functions.
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <numeric>
+#include <thread>
+#include <vector>
+
+#include "context.h"
+
+namespace {
+
+std::mutex g_err_mu;
+std::string g_err;
+
+void set_err(hb_context* c, const std::string& s) {
+  if (c) c->last_error = s;
+  std::lock_guard<std::mutex> lk(g_err_mu);
+  g_err = s;
+}
+
+template <typename F>
+hb_status guarded(hb_context* c, F&& f) {
+  try {
+    f();
+    return HB_OK;
+  } catch (const hb::Error& e) {
+    set_err(c, e.what());
+    return e.status;
+  } catch (const std::bad_alloc& e) {
+    set_err(c, "host allocation failed");
+    return HB_ENOMEM;
+  } catch (const std::exception& e) {
+    set_err(c, e.what());
+    return HB_ECUDA;
+  } catch (...) {
+    set_err(c, "unknown exception");
+    return HB_ECUDA;
+  }
+}
+
+using hb::Error;
+
+void check_kernel(const hb_kernel* k) {
+  if (!k) throw Error(HB_EINVAL, "kernel descriptor is NULL");
+  if (k->id < 0 || k->id > HB_K_CUSTOM) throw Error(HB_EINVAL, "unknown kernel id");
+  if (k->id == HB_K_CUSTOM)  // kernel.hpp:69-76: std::function cannot cross to the device
+    throw Error(HB_EUNSUPPORTED, "Custom kernels (std::function) are not supported on the device");
+  if (k->id == HB_K_HANKEL_H12_RE || k->id == HB_K_HANKEL_H12_IM)
+    throw Error(HB_EUNSUPPORTED, "J2/Y2 (bessel.hpp) are not on the device path");
+}
+
+// integer d-th root of n, or -1
+int64_t int_root(int64_t n, int d) {
+  int64_t r = (int64_t)std::llround(std::pow((double)n, 1.0 / d));
+  for (int64_t c = std::max<int64_t>(1, r - 2); c <= r + 2; ++c) {
+    int64_t p = 1;
+    for (int k = 0; k < d; ++k) p *= c;
+    if (p == n) return c;
+  }
+  return -1;
+}
+
+void check_cube(const hb_cube& c) {
+  if (c.d < 1 || c.d > 8) throw Error(HB_EINVAL, "cube dimension must be in 1..8");
+  if (!(c.side > 0.0)) throw Error(HB_EINVAL, "HyperCube: side must be positive");  // geometry.hpp:22
+  for (int k = 0; k < c.d; ++k)
+    if (!std::isfinite(c.lower[k])) throw Error(HB_EINVAL, "cube corner must be finite");
+}
+
+int64_t check_points(const hb_cube& c, int64_t n, int mode) {
+  if (n < 1) throw Error(HB_EINVAL, "empty point set");  // kernel.hpp:171
+  if (mode == HB_POINTS_UNIFORM) return 0;
+  if (mode != HB_POINTS_GRID_INTERIOR && mode != HB_POINTS_GRID_CLOSED)
+    throw Error(HB_EINVAL, "unknown point mode");
+  const int64_t m = int_root(n, c.d);
+  if (m < 1) throw Error(HB_EINVAL, "grid mode needs N = n^d (SPEC.md:540)");
+  if (mode == HB_POINTS_GRID_CLOSED && m < 2) throw Error(HB_EINVAL, "closed grid needs n >= 2");
+  return m;
+}
+
+void check_pair(const hb_pair* p) {
+  if (!p) throw Error(HB_EINVAL, "pair descriptor is NULL");
+  check_cube(p->target);
+  check_cube(p->source);
+  if (p->target.d != p->source.d) throw Error(HB_EINVAL, "point dimensions differ");  // kernel.hpp:172
+  check_points(p->target, p->n_target, p->point_mode);
+  check_points(p->source, p->n_source, p->point_mode);
+}
+
+void check_tols(const double* tols, int32_t ntol) {
+  if (!tols || ntol < 1 || ntol > HB_MAX_TOLS) throw Error(HB_EINVAL, "need 1..4 tolerances");
+  for (int t = 0; t < ntol; ++t)
+    if (!(tols[t] > 0.0 && tols[t] < 1.0)) throw Error(HB_EINVAL, "tolerance must be in (0, 1)");
+}
+
+unsigned int read_flags(hb_context* c, unsigned int* dflags) {
+  unsigned int f = 0;
+  HB_CUDA(cudaMemcpyAsync(c->pinned, dflags, sizeof(f), cudaMemcpyDeviceToHost, c->stream));
+  HB_CUDA(cudaStreamSynchronize(c->stream));
+  std::memcpy(&f, c->pinned, sizeof(f));
+  return f;
+}
+
+void raise_flags(unsigned int f) {
+  if (f & 1u)
+    throw Error(HB_ESINGULAR,
+                "kernel eval: r == 0 on a singular kernel with no diagonal value");  // kernel.hpp:152-153
+  if (f & 2u) throw Error(HB_EDOMAIN, "non-finite kernel entries");
+}
+
+void gen_points(hb_context* c, const hb_pair* pair, double* dt, double* ds) {
+  const int64_t mt = check_points(pair->target, pair->n_target, pair->point_mode);
+  const int64_t ms = check_points(pair->source, pair->n_source, pair->point_mode);
+  hb::launch_points(pair->target, pair->n_target, pair->point_mode, mt, pair->seed, 0, dt, c->stream);
+  hb::launch_points(pair->source, pair->n_source, pair->point_mode, ms, pair->seed, 1, ds, c->stream);
+}
+
+void rank_pair(hb_context* c, const hb_kernel* kernel, const hb_pair* pair, const double* tols,
+               int32_t ntol, hb_rank_result* out) {
+  check_kernel(kernel);
+  check_pair(pair);
+  check_tols(tols, ntol);
+  HB_CUDA(cudaSetDevice(c->device));
+  const int d = pair->target.d;
+  const int64_t m = pair->n_target, n = pair->n_source;
+  const int64_t lda = hb::round_up(m, 8);
+  size_t free_b = 0, total_b = 0;
+  HB_CUDA(cudaMemGetInfo(&free_b, &total_b));
+  if ((double)lda * n * 8.0 * 1.25 > (double)total_b)
+    throw Error(HB_ENOMEM, "K does not fit in device memory");
+  HB_CUDA(cudaEventRecord(c->ev[0], c->stream));
+  double* X = hb::ws<double>(c, hb::B_X, (size_t)d * m);
+  double* Yp = hb::ws<double>(c, hb::B_Y, (size_t)d * n);
+  double* A = hb::ws<double>(c, hb::B_A, (size_t)lda * n);
+  unsigned int* flags = hb::ws<unsigned int>(c, hb::B_FLAGS, 4);
+  HB_CUDA(cudaMemsetAsync(flags, 0, sizeof(unsigned int), c->stream));
+  gen_points(c, pair, X, Yp);
+  hb::launch_assemble(*kernel, X, m, Yp, n, d, A, lda, flags, c->stream);
+  HB_CUDA(cudaEventRecord(c->ev[4], c->stream));
+  raise_flags(read_flags(c, flags));
+  float fm = 0, cm = 0;
+  hb::rank_matrix_inplace(c, A, m, n, lda, tols, ntol, out, &fm, &cm);
+  float am = 0;
+  HB_CUDA(cudaEventElapsedTime(&am, c->ev[0], c->ev[4]));
+  for (int t = 0; t < ntol; ++t) {
+    out[t].sec[0] = am * 1e-3;
+    out[t].sec[3] = (am + fm + cm) * 1e-3;
+  }
+}
+
+// ---- cost model for the LPT partition --------------------------------
+double predicted_rank(int d, int dprime, int64_t n) {
+  // growth laws: far-field constant, vertex ~ log N, d'-surface ~ N^{d'/d};
+  // magnitudes from the paper tables at their first N row (F1/F2/F8 average).
+  static const double far_r[5] = {0, 7, 35, 100, 620};
+  static const double vert_r[5] = {0, 20, 60, 135, 375};
+  const double lg = std::log2(std::max<double>((double)n, 2.0) / 1000.0);
+  if (dprime < 0) return far_r[std::min(d, 4)];
+  if (dprime == 0) return vert_r[std::min(d, 4)] * (1.0 + 0.08 * std::max(0.0, lg));
+  const double n0 = d == 2 ? 1600.0 : (d == 3 ? 1000.0 : 1296.0);
+  double base = 200.0;
+  if (d == 3) base = dprime == 1 ? 105.0 : 330.0;
+  if (d >= 4) base = dprime == 1 ? 470.0 : (dprime == 2 ? 620.0 : 830.0);
+  return std::min<double>((double)n, base * std::pow((double)n / n0, (double)dprime / d));
+}
+
+double problem_cost(const hb_problem& p) {
+  const double n = (double)std::max(p.pair.n_target, p.pair.n_source);
+  const double pr = std::min(n, 1.4 * predicted_rank(p.pair.target.d, p.pair.d_prime, (int64_t)n) + 32.0);
+  return n * n * (60.0 + 4.0 * pr) + 30.0 * pr * pr * pr;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* hb_version(void) { return "hb200 0.1 (sm_100a)"; }
+
+const char* hb_status_string(hb_status s) {
+  switch (s) {
+    case HB_OK: return "ok";
+    case HB_EINVAL: return "invalid argument";
+    case HB_EDOMAIN: return "domain error";
+    case HB_ECAP: return "size cap exceeded";
+    case HB_ESINGULAR: return "singular kernel at r == 0";
+    case HB_EUNSUPPORTED: return "unsupported";
+    case HB_ENOMEM: return "out of memory";
+    case HB_ECUDA: return "CUDA error";
+    case HB_ENCCL: return "NCCL error";
+  }
+  return "unknown status";
+}
+
+const char* hb_last_error(const hb_context* ctx) {
+  if (ctx) return ctx->last_error.c_str();
+  std::lock_guard<std::mutex> lk(g_err_mu);
+  static thread_local std::string copy;
+  copy = g_err;
+  return copy.c_str();
+}
+
+hb_status hb_context_create(int device, hb_context** out) {
+  if (!out) return HB_EINVAL;
+  *out = nullptr;
+  hb_context* c = new (std::nothrow) hb_context();
+  if (!c) return HB_ENOMEM;
+  hb_status s = guarded(nullptr, [&] {
+    int n = 0;
+    HB_CUDA(cudaGetDeviceCount(&n));
+    if (device < 0 || device >= n) throw Error(HB_EINVAL, "no such CUDA device");
+    hb::context_init(c, device);
+  });
+  if (s != HB_OK) {
+    hb::context_free(c);
+    delete c;
+    return s;
+  }
+  *out = c;
+  return HB_OK;
+}
+
+void hb_context_destroy(hb_context* ctx) {
+  if (!ctx) return;
+  hb::context_free(ctx);
+  delete ctx;
+}
+
+void* hb_context_stream(hb_context* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
+
+hb_status hb_context_set_tuning(hb_context* ctx, int32_t block_max, double eta) {
+  if (!ctx) return HB_EINVAL;
+  if (block_max < 8 || block_max > hb::kBlockMax || block_max % 8) return HB_EINVAL;
+  if (!(eta > 0.0 && eta <= 0.1)) return HB_EINVAL;
+  ctx->block_max = block_max;
+  ctx->eta = eta;
+  return HB_OK;
+}
+
+hb_status hb_generate_points(hb_context* ctx, const hb_pair* pair, double* d_tgt, double* d_src) {
+  if (!ctx) return HB_EINVAL;
+  return guarded(ctx, [&] {
+    check_pair(pair);
+    if (!d_tgt || !d_src) throw Error(HB_EINVAL, "NULL output buffer");
+    HB_CUDA(cudaSetDevice(ctx->device));
+    gen_points(ctx, pair, d_tgt, d_src);
+  });
+}
+
+hb_status hb_assemble(hb_context* ctx, const hb_kernel* kernel, const double* d_tgt, int64_t T,
+                      const double* d_src, int64_t N, int32_t d, double* d_K, int64_t ldk) {
+  if (!ctx) return HB_EINVAL;
+  return guarded(ctx, [&] {
+    check_kernel(kernel);
+    if (T <= 0 || N <= 0) throw Error(HB_EINVAL, "assemble_dense: empty point set");  // kernel.hpp:171
+    if (d < 1 || d > 8) throw Error(HB_EINVAL, "assemble_dense: bad dimension");
+    if (ldk < T) throw Error(HB_EINVAL, "assemble_dense: ldk < T");
+    if (!d_tgt || !d_src || !d_K) throw Error(HB_EINVAL, "NULL buffer");
+    HB_CUDA(cudaSetDevice(ctx->device));
+    unsigned int* flags = hb::ws<unsigned int>(ctx, hb::B_FLAGS, 4);
+    HB_CUDA(cudaMemsetAsync(flags, 0, sizeof(unsigned int), ctx->stream));
+    hb::launch_assemble(*kernel, d_tgt, T, d_src, N, d, d_K, ldk, flags, ctx->stream);
+    raise_flags(read_flags(ctx, flags));
+  });
+}
+
+hb_status hb_eval_radial_host(const hb_kernel* k, double r, double* out) {
+  return guarded(nullptr, [&] {
+    check_kernel(k);
+    if (!out) throw Error(HB_EINVAL, "NULL output");
+    if (r == 0.0) {  // kernel.hpp:150-155
+      if (k->has_diag) { *out = k->diag; return; }
+      if (hb::kernel_singular_at_origin(k->id))
+        throw Error(HB_ESINGULAR, "kernel eval: r == 0 on a singular kernel with no diagonal value");
+    }
+    switch (k->id) {  // kernel.hpp:93-109
+      case HB_K_INVERSE_R: *out = 1.0 / r; break;
+      case HB_K_LOG_R: *out = std::log(r); break;
+      case HB_K_HELMHOLTZ3D_RE: *out = std::cos(r) / r; break;
+      case HB_K_HELMHOLTZ3D_IM: *out = std::sin(r) / r; break;
+      case HB_K_R: *out = r; break;
+      case HB_K_SIN_R: *out = std::sin(r); break;
+      case HB_K_INV_SQRT_1_PLUS_R: *out = 1.0 / std::sqrt(1.0 + r); break;
+      case HB_K_EXP_NEG_R: *out = std::exp(-r); break;
+      case HB_K_EXP_NEG_R2: *out = std::exp(-(r * r)); break;
+      default: throw Error(HB_EUNSUPPORTED, "kernel not available");
+    }
+  });
+}
+
+hb_status hb_rank_matrix(hb_context* ctx, const double* d_A, int64_t m, int64_t n, int64_t ld,
+                         const double* tols, int32_t ntol, hb_rank_result* out) {
+  if (!ctx) return HB_EINVAL;
+  return guarded(ctx, [&] {
+    if (m < 1 || n < 1) throw Error(HB_EINVAL, "epsilon_rank: empty matrix");
+    if (ld < m || !d_A || !out) throw Error(HB_EINVAL, "bad matrix arguments");
+    check_tols(tols, ntol);
+    HB_CUDA(cudaSetDevice(ctx->device));
+    const int64_t lda = hb::round_up(m, 8);
+    double* A = hb::ws<double>(ctx, hb::B_A, (size_t)lda * n);
+    HB_CUDA(cudaMemcpy2DAsync(A, lda * 8, d_A, ld * 8, m * 8, n, cudaMemcpyDeviceToDevice, ctx->stream));
+    unsigned int* flags = hb::ws<unsigned int>(ctx, hb::B_FLAGS, 4);
+    HB_CUDA(cudaMemsetAsync(flags, 0, sizeof(unsigned int), ctx->stream));
+    hb::nonfinite_kernel<<<(unsigned)hb::ceil_div(m * n, 256), 256, 0, ctx->stream>>>(A, m, n, lda, flags);
+    HB_LAUNCH_CHECK();
+    raise_flags(read_flags(ctx, flags));  // SPEC.md:564 non-finite entries -> numeric error
+    float fm = 0, cm = 0;
+    hb::rank_matrix_inplace(ctx, A, m, n, lda, tols, ntol, out, &fm, &cm);
+    for (int t = 0; t < ntol; ++t) out[t].sec[3] = (fm + cm) * 1e-3;
+  });
+}
+
+hb_status hb_rank(hb_context* ctx, const hb_kernel* kernel, const hb_pair* pair, const double* tols,
+                  int32_t ntol, hb_rank_result* out) {
+  if (!ctx || !out) return HB_EINVAL;
+  return guarded(ctx, [&] { rank_pair(ctx, kernel, pair, tols, ntol, out); });
+}
+
+hb_status hb_last_sigma(hb_context* ctx, double* host_out, int64_t max, int64_t* count) {
+  if (!ctx || !count) return HB_EINVAL;
+  return guarded(ctx, [&] {
+    const int64_t k = ctx->last_k;
+    *count = k;
+    if (k == 0 || max <= 0 || !host_out) return;
+    HB_CUDA(cudaSetDevice(ctx->device));
+    double* d = hb::ws<double>(ctx, hb::B_D, (size_t)k + 1);
+    double* e = hb::ws<double>(ctx, hb::B_E, (size_t)k + 1);
+    double* o = hb::ws<double>(ctx, hb::B_BV, (size_t)2 * k + 8);
+    hb::sigma_all_kernel<<<(unsigned)hb::ceil_div(k * 32, 256), 256, 0, ctx->stream>>>(
+        d, e, k, ctx->last_sigma1, o);
+    HB_LAUNCH_CHECK();
+    const int64_t cnt = std::min(k, max);
+    HB_CUDA(cudaMemcpyAsync(host_out, o, cnt * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    HB_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+uint64_t hb_problem_seed(uint64_t base, int32_t d, int32_t d_prime, int64_t n) {
+  const uint64_t key = ((uint64_t)d << 48) | ((uint64_t)(d_prime + 1) << 40) | (uint64_t)n;
+  return hb::splitmix64(base ^ hb::splitmix64(key));
+}
+
+hb_status hb_partition(const hb_problem* probs, int64_t n, int32_t nparts, int32_t* owner) {
+  if ((!probs && n > 0) || nparts < 1 || (!owner && n > 0) || n < 0) return HB_EINVAL;
+  std::vector<int64_t> order(n);
+  std::iota(order.begin(), order.end(), 0);
+  std::vector<double> cost(n);
+  for (int64_t i = 0; i < n; ++i) cost[i] = problem_cost(probs[i]);
+  std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) { return cost[a] > cost[b]; });
+  std::vector<double> load(nparts, 0.0);
+  for (int64_t i : order) {
+    int best = 0;
+    for (int p = 1; p < nparts; ++p)
+      if (load[p] < load[best]) best = p;
+    owner[i] = best;
+    load[best] += cost[i];
+  }
+  return HB_OK;
+}
+
+hb_status hb_sweep(const hb_problem* probs, int64_t n, const int32_t* devices, int32_t ndev,
+                   hb_rank_result* out, int32_t* status_out) {
+  if (n < 0 || (n > 0 && (!probs || !out)) || ndev < 1 || !devices) return HB_EINVAL;
+  std::vector<int64_t> offset(n + 1, 0);
+  for (int64_t i = 0; i < n; ++i) {
+    if (probs[i].ntol < 1 || probs[i].ntol > HB_MAX_TOLS) return HB_EINVAL;
+    offset[i + 1] = offset[i] + probs[i].ntol;
+  }
+  std::vector<int32_t> owner(n);
+  hb_partition(probs, n, ndev, owner.data());
+  std::vector<hb_status> st(n, HB_OK);
+  std::vector<double> cost(n);
+  for (int64_t i = 0; i < n; ++i) cost[i] = problem_cost(probs[i]);
+  std::vector<hb_status> dev_status(ndev, HB_OK);
+  auto worker = [&](int w) {
+    hb_context* c = nullptr;
+    hb_status s = hb_context_create(devices[w], &c);
+    if (s != HB_OK) {
+      dev_status[w] = s;
+      for (int64_t i = 0; i < n; ++i)
+        if (owner[i] == w) st[i] = s;
+      return;
+    }
+    std::vector<int64_t> mine;
+    for (int64_t i = 0; i < n; ++i)
+      if (owner[i] == w) mine.push_back(i);
+    std::stable_sort(mine.begin(), mine.end(), [&](int64_t a, int64_t b) { return cost[a] > cost[b]; });
+    for (int64_t i : mine) {
+      const hb_problem& p = probs[i];
+      st[i] = hb_rank(c, &p.kernel, &p.pair, p.tols, p.ntol, out + offset[i]);
+    }
+    hb_context_destroy(c);
+  };
+  std::vector<std::thread> th;
+  for (int w = 1; w < ndev; ++w) th.emplace_back(worker, w);
+  worker(0);
+  for (auto& t : th) t.join();
+  hb_status first = HB_OK;
+  for (int64_t i = 0; i < n; ++i) {
+    if (status_out) status_out[i] = st[i];
+    if (first == HB_OK && st[i] != HB_OK) first = st[i];
+  }
+  return first;
+}
+
+}  // extern "C"
+
+#include "hb_debug.h"
+
+extern "C" hb_status hb_debug_dgemm_async(hb_context* ctx, int32_t transA, int64_t M, int64_t N,
+                                          int64_t K, double alpha, const double* A, int64_t lda,
+                                          const double* B, int64_t ldb, double beta, double* C,
+                                          int64_t ldc, int32_t reps) {
+  if (!ctx) return HB_EINVAL;
+  return guarded(ctx, [&] {
+    if (M < 0 || N < 0 || K < 0) throw Error(HB_EINVAL, "negative size");
+    HB_CUDA(cudaSetDevice(ctx->device));
+    hb::GemmArgs g{};
+    g.M = M; g.N = N; g.K = K; g.alpha = alpha; g.A = A; g.lda = lda; g.transA = transA != 0;
+    g.B = B; g.ldb = ldb; g.beta = beta; g.C = C; g.ldc = ldc;
+    const int64_t wse = 8ll << 20;
+    double* sk = hb::ws<double>(ctx, hb::B_SPLITK, wse);
+    for (int r = 0; r < reps; ++r) hb::launch_dgemm(g, sk, wse, ctx->num_sms, ctx->stream);
+  });
+}
+
+extern "C" hb_status hb_debug_dgemm(hb_context* ctx, int32_t transA, int64_t M, int64_t N, int64_t K,
+                                    double alpha, const double* A, int64_t lda, const double* B,
+                                    int64_t ldb, double beta, double* C, int64_t ldc) {
+  hb_status s = hb_debug_dgemm_async(ctx, transA, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, 1);
+  if (s != HB_OK) return s;
+  return guarded(ctx, [&] { HB_CUDA(cudaStreamSynchronize(ctx->stream)); });
+}

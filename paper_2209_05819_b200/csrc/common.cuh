@@ -1,0 +1,98 @@
+// Shared device/host helpers for the hb200 rank-reveal path (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <stdexcept>
+#include <string>
+
+#include "hb.h"
+
+namespace hb {
+
+// Error carrying an hb_status; converted to a status code at the C ABI (abi.cpp).
+struct Error : std::runtime_error {
+  hb_status status;
+  Error(hb_status s, const std::string& what) : std::runtime_error(what), status(s) {}
+};
+
+#define HB_CUDA(x)                                                                           \
+  do {                                                                                       \
+    cudaError_t e_ = (x);                                                                    \
+    if (e_ != cudaSuccess)                                                                   \
+      throw ::hb::Error(e_ == cudaErrorMemoryAllocation ? HB_ENOMEM : HB_ECUDA,              \
+                        std::string(#x) + ": " + cudaGetErrorString(e_) + " @" __FILE__ ":" + \
+                            std::to_string(__LINE__));                                       \
+  } while (0)
+
+#define HB_LAUNCH_CHECK() HB_CUDA(cudaGetLastError())
+
+#define HB_REQUIRE(cond, st, msg) \
+  do {                            \
+    if (!(cond)) throw ::hb::Error(st, msg); \
+  } while (0)
+
+constexpr int kSketchRows = 128;  // ℓ: sketch rows (block size cap + oversampling)
+constexpr int kBlockMax = 120;    // largest pivot block b (multiple of 8, ℓ - b >= 8)
+
+__host__ __device__ inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+__host__ __device__ inline int64_t ceil_div(int64_t x, int64_t m) { return (x + m - 1) / m; }
+
+__host__ __device__ inline uint64_t splitmix64(uint64_t x) {
+  uint64_t z = x + 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+// ---------------------------------------------------------------------------------------------
+// Grid-wide barrier for cooperative (co-resident) launches.  State = {count, generation}; the
+// count self-resets, the generation grows monotonically, so no reset between launches is needed
+// as long as every launch uses the same gridDim for a given state slot.
+// ---------------------------------------------------------------------------------------------
+struct GridBarrier {
+  unsigned int* count;
+  unsigned int* gen;
+};
+
+__device__ __forceinline__ void grid_sync(GridBarrier b) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned int* vgen = b.gen;
+    const unsigned int my_gen = *vgen;
+    __threadfence();
+    const unsigned int nb = gridDim.x * gridDim.y * gridDim.z;
+    const unsigned int arrived = atomicAdd(b.count, 1u);
+    if (arrived == nb - 1) {
+      *b.count = 0;
+      __threadfence();
+      atomicAdd(b.gen, 1u);
+    } else {
+      while (*vgen == my_gen) __nanosleep(20);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Block-wide sum; result valid in all threads. smem must hold >= 32 doubles.
+__device__ __forceinline__ double block_sum(double v, double* smem) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int nw = (blockDim.x + 31) >> 5;
+  v = warp_sum(v);
+  __syncthreads();
+  if (lane == 0) smem[wid] = v;
+  __syncthreads();
+  double t = 0.0;
+  for (int w = 0; w < nw; ++w) t += smem[w];  // fixed order: deterministic
+  return t;
+}
+
+}  // namespace hb

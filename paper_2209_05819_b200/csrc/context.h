@@ -1,0 +1,62 @@
+// hb_context: per-device, per-host-thread state (stream, workspace, barrier slot).
+#pragma once
+
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "kernels.h"
+#include "qr.h"
+
+struct hb_context {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int num_sms = 148;
+  int block_max = hb::kBlockMax;
+  double eta = 0.01;  // stop once ||A22||_F <= eta * tol * sigma1
+  unsigned int* bar = nullptr;  // {count, gen}
+  double* pinned = nullptr;     // small host staging (pinned)
+  std::string last_error;
+
+  struct Buf {
+    void* p = nullptr;
+    size_t cap = 0;
+  };
+  std::vector<Buf> bufs;
+  cudaEvent_t ev[6] = {};
+
+  // last certification (for hb_last_sigma)
+  int64_t last_k = 0;
+  double last_sigma1 = 0.0;
+};
+
+namespace hb {
+
+enum BufId {
+  B_A, B_X, B_Y, B_OMEGA, B_YSK, B_YS, B_NRM, B_V, B_W, B_W2, B_S, B_T, B_Z, B_TAU, B_SLOTS,
+  B_PIV, B_SWAPS, B_RDIAG, B_EST, B_BEFF, B_PERM, B_FRO, B_FROSUM, B_SPLITK, B_CERT_B, B_CERT_M,
+  B_D, B_E, B_BW, B_BV, B_SCAL, B_FLAGS, B_QUERY, B_ANSWER, B_SIG1, B_COUNT
+};
+
+template <typename T>
+T* ws(hb_context* c, int id, size_t elems) {
+  if ((int)c->bufs.size() <= id) c->bufs.resize(B_COUNT);
+  auto& b = c->bufs[id];
+  const size_t bytes = std::max<size_t>(elems, 1) * sizeof(T);
+  if (b.cap < bytes) {
+    if (b.p) HB_CUDA(cudaFreeAsync(b.p, c->stream));
+    const size_t nb = bytes + bytes / 8;  // headroom
+    HB_CUDA(cudaMallocAsync(&b.p, nb, c->stream));
+    b.cap = nb;
+  }
+  return static_cast<T*>(b.p);
+}
+
+// Internal entry points (rank.cu).
+void rank_matrix_inplace(hb_context* c, double* A, int64_t m, int64_t n, int64_t lda,
+                         const double* tols, int ntol, hb_rank_result* out, float* fact_ms,
+                         float* cert_ms);
+void context_init(hb_context* c, int device);
+void context_free(hb_context* c);
+
+}  // namespace hb

@@ -1,0 +1,319 @@
+// FP64 GEMM on the sm_100a double-precision tensor path (mma.sync m8n8k4 f64 -> SASS DMMA).
+//
+// tcgen05 has no f64 kind, so FP64 tensor work on B200 goes through the legacy warp-level
+// mma.sync; the probe in tools/fp64_peak.cu measured DMMA = DFMA = 36.9 TF/s on this pool.
+// Used for every dense contraction of the rank-reveal: the sketch Y = Ω·A, the compact-WY
+// trailing update W = Vᵀ·A2, W ← Tᵀ·W, A2 −= V·W, the sketch downdate Y2 −= Z·R12, and the same
+// shapes inside the certification QR.
+//
+// Tiling: 256 threads (8 warps), CTA tile BM x BN x 16, 3-stage cp.async pipeline, padded
+// shared-memory layouts chosen so every fragment load is bank-conflict free:
+//   A (N-mode, M x K col-major): As[k][m] with row stride BM+4   (m contiguous)
+//   A (T-mode, K x M col-major): As[m][k] with row stride 16+4   (k contiguous)
+//   B (K x N col-major):         Bs[n][k] with row stride 16+4   (k contiguous)
+// m8n8k4 fragments: a = A[m=lane/4][k=lane%4], b = B[k=lane%4][n=lane/4],
+//                   c = C[m=lane/4][n=2*(lane%4)+{0,1}].
+// Optional epilogue: per-CTA sum of squares of the updated C below a row offset (the exact
+// Frobenius norm of the trailing matrix A22, used by the QR stopping rule), written in a fixed
+// order so the result is deterministic.  Split-K (for skinny outputs with a long reduction)
+// writes per-slice partials that a second kernel sums in a fixed order.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace hb {
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void cp_async16(unsigned dst, const void* src, int bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(bytes));
+}
+__device__ __forceinline__ void cp_async8(unsigned dst, const void* src, int bytes) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst), "l"(src), "r"(bytes));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1},{%2},{%3},{%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+struct GemmParams {
+  int64_t M, N, K;
+  double alpha, beta;
+  const double* A;
+  int64_t lda;
+  const double* B;
+  int64_t ldb;
+  double* C;
+  int64_t ldc;
+  double* partial;  // split-K slices (M x N each, ld = M) or nullptr
+  int64_t kchunk;
+  double* fro;      // per-CTA Frobenius partials or nullptr
+  int64_t fro_row0;
+};
+
+template <bool TA, int WARPS_M, int WARPS_N, int WM, int WN>
+struct Cfg {
+  static constexpr int BM = WARPS_M * WM * 8;
+  static constexpr int BN = WARPS_N * WN * 8;
+  static constexpr int BK = 16;
+  static constexpr int STAGES = 3;
+  static constexpr int AS = TA ? (BK + 4) : (BM + 4);  // A row stride
+  static constexpr int A_ELEMS = TA ? BM * (BK + 4) : BK * (BM + 4);
+  static constexpr int B_ELEMS = BN * (BK + 4);
+  static constexpr int SMEM = STAGES * (A_ELEMS + B_ELEMS) * 8;
+};
+
+template <bool TA, int WARPS_M, int WARPS_N, int WM, int WN, bool VEC>
+__global__ void __launch_bounds__(256, 1) dgemm_kernel(GemmParams p) {
+  using C_ = Cfg<TA, WARPS_M, WARPS_N, WM, WN>;
+  constexpr int BM = C_::BM, BN = C_::BN, BK = C_::BK, STAGES = C_::STAGES;
+  extern __shared__ __align__(16) double smem[];
+  double* As = smem;
+  double* Bs = smem + STAGES * C_::A_ELEMS;
+  __shared__ double red[32];
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp % WARPS_M, wn = warp / WARPS_M;
+  const int64_t m0 = (int64_t)blockIdx.x * BM, n0 = (int64_t)blockIdx.y * BN;
+  const int64_t kbeg = (int64_t)blockIdx.z * p.kchunk;
+  const int64_t kend = min(p.K, kbeg + p.kchunk);
+  const int nk = kend > kbeg ? (int)((kend - kbeg + BK - 1) / BK) : 0;
+
+  auto load_tile = [&](int kt, int stage) {
+    const int64_t k0 = kbeg + (int64_t)kt * BK;
+    double* as = As + stage * C_::A_ELEMS;
+    double* bs = Bs + stage * C_::B_ELEMS;
+    if (!TA) {
+      constexpr int VPC = BM / 2;
+      for (int v = tid; v < BK * VPC; v += 256) {
+        const int kk = v / VPC, mm = (v % VPC) * 2;
+        const int64_t gm = m0 + mm, gk = k0 + kk;
+        const double* src = p.A + gm + gk * p.lda;
+        double* dst = as + kk * (BM + 4) + mm;
+        if (VEC) {
+          int bytes = 0;
+          if (gk < kend) bytes = gm + 1 < p.M ? 16 : (gm < p.M ? 8 : 0);
+          cp_async16(smem_u32(dst), bytes ? src : p.A, bytes);
+        } else {
+          const bool v0 = gk < kend && gm < p.M, v1 = gk < kend && gm + 1 < p.M;
+          cp_async8(smem_u32(dst), v0 ? src : p.A, v0 ? 8 : 0);
+          cp_async8(smem_u32(dst + 1), v1 ? src + 1 : p.A, v1 ? 8 : 0);
+        }
+      }
+    } else {
+      constexpr int VPR = BK / 2;
+      for (int v = tid; v < BM * VPR; v += 256) {
+        const int mm = v / VPR, kk = (v % VPR) * 2;
+        const int64_t gm = m0 + mm, gk = k0 + kk;
+        const double* src = p.A + gk + gm * p.lda;
+        double* dst = as + mm * (BK + 4) + kk;
+        if (VEC) {
+          int bytes = 0;
+          if (gm < p.M) bytes = gk + 1 < kend ? 16 : (gk < kend ? 8 : 0);
+          cp_async16(smem_u32(dst), bytes ? src : p.A, bytes);
+        } else {
+          const bool v0 = gm < p.M && gk < kend, v1 = gm < p.M && gk + 1 < kend;
+          cp_async8(smem_u32(dst), v0 ? src : p.A, v0 ? 8 : 0);
+          cp_async8(smem_u32(dst + 1), v1 ? src + 1 : p.A, v1 ? 8 : 0);
+        }
+      }
+    }
+    {
+      constexpr int VPR = BK / 2;
+      for (int v = tid; v < BN * VPR; v += 256) {
+        const int nn = v / VPR, kk = (v % VPR) * 2;
+        const int64_t gn = n0 + nn, gk = k0 + kk;
+        const double* src = p.B + gk + gn * p.ldb;
+        double* dst = bs + nn * (BK + 4) + kk;
+        if (VEC) {
+          int bytes = 0;
+          if (gn < p.N) bytes = gk + 1 < kend ? 16 : (gk < kend ? 8 : 0);
+          cp_async16(smem_u32(dst), bytes ? src : p.B, bytes);
+        } else {
+          const bool v0 = gn < p.N && gk < kend, v1 = gn < p.N && gk + 1 < kend;
+          cp_async8(smem_u32(dst), v0 ? src : p.B, v0 ? 8 : 0);
+          cp_async8(smem_u32(dst + 1), v1 ? src + 1 : p.B, v1 ? 8 : 0);
+        }
+      }
+    }
+  };
+
+  double acc[WM][WN][2];
+#pragma unroll
+  for (int i = 0; i < WM; ++i)
+#pragma unroll
+    for (int j = 0; j < WN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < nk) load_tile(s, s);
+    cp_commit();
+  }
+  const int ar = lane >> 2, ac = lane & 3;
+  for (int kt = 0; kt < nk; ++kt) {
+    cp_wait<STAGES - 2>();
+    __syncthreads();
+    {
+      const int pf = kt + STAGES - 1;
+      if (pf < nk) load_tile(pf, pf % STAGES);
+      cp_commit();
+    }
+    const double* as = As + (kt % STAGES) * C_::A_ELEMS;
+    const double* bs = Bs + (kt % STAGES) * C_::B_ELEMS;
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      double a[WM], b[WN];
+#pragma unroll
+      for (int i = 0; i < WM; ++i) {
+        const int m = (wm * WM + i) * 8 + ar;
+        a[i] = TA ? as[m * (BK + 4) + kk + ac] : as[(kk + ac) * (BM + 4) + m];
+      }
+#pragma unroll
+      for (int j = 0; j < WN; ++j) {
+        const int n = (wn * WN + j) * 8 + ar;
+        b[j] = bs[n * (BK + 4) + kk + ac];
+      }
+#pragma unroll
+      for (int i = 0; i < WM; ++i)
+#pragma unroll
+        for (int j = 0; j < WN; ++j) dmma884(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+    }
+  }
+  cp_wait<0>();
+
+  double fro = 0.0;
+#pragma unroll
+  for (int i = 0; i < WM; ++i) {
+    const int64_t m = m0 + (wm * WM + i) * 8 + ar;
+    if (m >= p.M) continue;
+#pragma unroll
+    for (int j = 0; j < WN; ++j) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int64_t n = n0 + (wn * WN + j) * 8 + 2 * ac + h;
+        if (n >= p.N) continue;
+        const double v = p.alpha * acc[i][j][h];
+        if (p.partial) {
+          p.partial[(int64_t)blockIdx.z * p.M * p.N + m + n * p.M] = v;
+        } else {
+          double* c = p.C + m + n * p.ldc;
+          const double out = p.beta == 0.0 ? v : v + p.beta * *c;
+          *c = out;
+          if (m >= p.fro_row0) fro += out * out;
+        }
+      }
+    }
+  }
+  if (p.fro && !p.partial) {
+    const double s = block_sum(fro, red);
+    if (tid == 0) p.fro[(int64_t)blockIdx.y * gridDim.x + blockIdx.x] = s;
+  }
+}
+
+// Split-K finish: C = sum_z P[z] + beta*C (fixed order), optional Frobenius partials.
+__global__ void splitk_reduce(GemmParams p, int slices) {
+  __shared__ double red[32];
+  const int64_t total = p.M * p.N;
+  double fro = 0.0;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t m = idx % p.M, n = idx / p.M;
+    double s = 0.0;
+    for (int z = 0; z < slices; ++z) s += p.partial[(int64_t)z * total + idx];
+    double* c = p.C + m + n * p.ldc;
+    const double out = p.beta == 0.0 ? s : s + p.beta * *c;
+    *c = out;
+    if (m >= p.fro_row0) fro += out * out;
+  }
+  if (p.fro) {
+    const double s = block_sum(fro, red);
+    if (threadIdx.x == 0) p.fro[blockIdx.x] = s;
+  }
+}
+
+template <bool TA, int WARPS_M, int WARPS_N, int WM, int WN>
+static void run_cfg(const GemmParams& p, int slices, bool vec, cudaStream_t st) {
+  using C_ = Cfg<TA, WARPS_M, WARPS_N, WM, WN>;
+  dim3 grid((unsigned)ceil_div(p.M, C_::BM), (unsigned)ceil_div(p.N, C_::BN), (unsigned)slices);
+  HB_REQUIRE(grid.y <= 65535u && grid.z <= 65535u, HB_ECAP, "dgemm: grid too large");
+  // the attribute is per device; setting it on every launch costs ~1 µs of host time
+  if (vec) {
+    auto k = dgemm_kernel<TA, WARPS_M, WARPS_N, WM, WN, true>;
+    HB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C_::SMEM));
+    k<<<grid, 256, C_::SMEM, st>>>(p);
+  } else {
+    auto k = dgemm_kernel<TA, WARPS_M, WARPS_N, WM, WN, false>;
+    HB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C_::SMEM));
+    k<<<grid, 256, C_::SMEM, st>>>(p);
+  }
+  HB_LAUNCH_CHECK();
+}
+
+static constexpr int kReduceBlocks = 592;  // 4 x 148 SMs
+
+static int64_t tiles_of(int64_t M, int64_t N) {
+  const int bm = M <= 64 ? 64 : 128;
+  return ceil_div(M, bm) * ceil_div(N, 128);
+}
+
+static int choose_slices(int64_t M, int64_t N, int64_t K, int num_sms, int64_t ws_elems) {
+  const int64_t tiles = tiles_of(M, N);
+  if (tiles >= num_sms || K < 1024) return 1;
+  int64_t s = ceil_div(2 * (int64_t)num_sms, tiles);
+  s = std::min<int64_t>(s, K / 512);
+  s = std::min<int64_t>(s, 32);
+  while (s > 1 && s * M * N > ws_elems) --s;
+  return (int)std::max<int64_t>(s, 1);
+}
+
+int64_t gemm_fro_count(int64_t M, int64_t N) { return std::max<int64_t>(tiles_of(M, N), kReduceBlocks); }
+
+void launch_dgemm(const GemmArgs& g, double* ws, int64_t ws_elems, int num_sms, cudaStream_t st) {
+  if (g.M <= 0 || g.N <= 0) return;
+  GemmParams p{};
+  p.M = g.M; p.N = g.N; p.K = g.K;
+  p.alpha = g.alpha; p.beta = g.beta;
+  p.A = g.A; p.lda = g.lda; p.B = g.B; p.ldb = g.ldb; p.C = g.C; p.ldc = g.ldc;
+  p.fro = g.fro_partials; p.fro_row0 = g.fro_row0;
+  if (g.K <= 0) {  // C = beta*C
+    p.partial = nullptr;
+    p.kchunk = 1;
+  }
+  const bool vec = (g.lda % 2 == 0) && (g.ldb % 2 == 0) &&
+                   ((reinterpret_cast<uintptr_t>(g.A) | reinterpret_cast<uintptr_t>(g.B)) & 15) == 0;
+  const int slices = g.K > 0 ? choose_slices(g.M, g.N, g.K, num_sms, ws ? ws_elems : 0) : 1;
+  p.kchunk = slices > 1 ? round_up(ceil_div(g.K, slices), 16) : std::max<int64_t>(g.K, 1);
+  const int s_eff = slices > 1 ? (int)ceil_div(g.K, p.kchunk) : 1;
+  GemmParams q = p;
+  if (s_eff > 1) {
+    q.partial = ws;
+    q.fro = nullptr;
+  }
+  if (g.M <= 64) {
+    if (g.transA) run_cfg<true, 1, 8, 8, 2>(q, s_eff, vec, st);
+    else run_cfg<false, 1, 8, 8, 2>(q, s_eff, vec, st);
+  } else {
+    if (g.transA) run_cfg<true, 2, 4, 8, 4>(q, s_eff, vec, st);
+    else run_cfg<false, 2, 4, 8, 4>(q, s_eff, vec, st);
+  }
+  if (s_eff > 1) {
+    p.partial = ws;
+    splitk_reduce<<<kReduceBlocks, 256, 0, st>>>(p, s_eff);
+    HB_LAUNCH_CHECK();
+  } else if (g.fro_partials) {
+    // pad the partial array to the fixed count with zeros so the consumer can always sum
+    // gemm_fro_count(M, N) entries
+    const int64_t written = tiles_of(g.M, g.N);
+    const int64_t cnt = gemm_fro_count(g.M, g.N);
+    if (cnt > written)
+      HB_CUDA(cudaMemsetAsync(g.fro_partials + written, 0, (cnt - written) * sizeof(double), st));
+  }
+}
+
+}  // namespace hb

@@ -1,0 +1,481 @@
+// k3: sketch-pivoted blocked Householder QR building blocks (sm_100a).
+//
+// This replaces SPEC `epsilon_rank` ("computes full singular values") with a
+// rank-revealing factorisation that only touches O(N^2 k) flops: HQRRP-style block pivoting.
+//   * Ω (ℓ x m, Gaussian, counter-based) sketches the trailing matrix: Y = Ω A (DMMA GEMM).
+//   * sketch_cpqr: column-pivoted Householder QR of the small ℓ x n sketch picks b pivots —
+//     warp-shuffle norm/argmax search, one grid barrier per pivot, norms recomputed exactly
+//     from the updated sketch column (the downdate is free because the column is in flight).
+//   * permute: the b chosen columns move to the front (LAPACK swap semantics) in A, Y, perm.
+//   * panel_qr: unpivoted Householder QR of the tall m x b panel (grid-cooperative, two grid
+//     barriers per column); emits the explicit V and τ; T of the compact-WY form Q = I − V T Vᵀ
+//     comes from S = VᵀV (DMMA GEMM) and the forward recurrence of LAPACK dlarft.
+//   * the trailing update A2 ← (I − V Tᵀ Vᵀ) A2 and the sketch downdate Y2 −= Y1 R11⁻¹ R12
+//     are DMMA GEMMs (dgemm.cu); Z = Y1 R11⁻¹ is a small triangular solve here.
+//   * power_sigma1: power iteration on the first b rows of R — a lower bound on σ₁ used for the
+//     stopping threshold before the certification computes σ₁ exactly.
+#include "common.cuh"
+#include "kernels.h"
+#include "qr.h"
+
+namespace hb {
+
+// ------------------------------------------------------------------------------------------
+// Gaussian Ω: entry (i, c) = Box–Muller of two counter hashes; deterministic in (seed, i, c).
+// ------------------------------------------------------------------------------------------
+__global__ void gaussian_kernel(double* __restrict__ om, int64_t rows, int64_t cols, int64_t ld,
+                                uint64_t seed) {
+  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= rows * cols) return;
+  const int64_t i = idx % rows, c = idx / rows;
+  const uint64_t h = splitmix64(seed ^ splitmix64((uint64_t)c * 0x100000001B3ull + (uint64_t)i));
+  const uint64_t h2 = splitmix64(h);
+  const double u1 = ((double)(h >> 11) + 0.5) * 0x1p-53;
+  const double u2 = (double)(h2 >> 11) * 0x1p-53;
+  om[i + c * ld] = sqrt(-2.0 * log(u1)) * cospi(2.0 * u2);
+}
+
+void launch_gaussian(double* om, int64_t rows, int64_t cols, int64_t ld, uint64_t seed,
+                     cudaStream_t st) {
+  const int64_t tot = rows * cols;
+  if (tot == 0) return;
+  gaussian_kernel<<<(unsigned)ceil_div(tot, 256), 256, 0, st>>>(om, rows, cols, ld, seed);
+  HB_LAUNCH_CHECK();
+}
+
+// ------------------------------------------------------------------------------------------
+// sketch_cpqr: b pivots from the ℓ x n_tr sketch.
+// ------------------------------------------------------------------------------------------
+__device__ __forceinline__ bool better(double na, int ia, double nb, int ib) {
+  return na > nb || (na == nb && ia < ib);
+}
+
+__global__ void __launch_bounds__(256) sketch_cpqr_kernel(SketchParams p) {
+  const int G = gridDim.x, g = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int ell = p.ell;
+  const int64_t cpc = ceil_div(p.n_tr, G);
+  const int64_t c0 = g * cpc, c1 = min(p.n_tr, c0 + cpc);
+  __shared__ double v[kSketchRows];
+  __shared__ double wbest[8], wsum[8];
+  __shared__ int wbi[8];
+  __shared__ double sh_tau;
+  __shared__ int sh_piv, sh_stop;
+
+  // init: copy Y -> Ys, exact column norms
+  double best = -1.0, sum = 0.0;
+  int bi = INT_MAX;
+  for (int64_t q = c0 + warp; q < c1; q += 8) {
+    double s = 0.0;
+    for (int i = lane; i < ell; i += 32) {
+      const double y = p.Y[i + q * p.ldy];
+      p.Ys[i + q * p.ldy] = y;
+      s += y * y;
+    }
+    s = warp_sum(s);
+    if (lane == 0) p.nrm[q] = s;
+    if (better(s, (int)q, best, bi)) { best = s; bi = (int)q; }
+    sum += s;
+  }
+  auto publish = [&](int slot) {
+    if (lane == 0) { wbest[warp] = best; wbi[warp] = bi; wsum[warp] = sum; }
+    __syncthreads();
+    if (tid == 0) {
+      double b0 = -1.0, s0 = 0.0;
+      int i0 = INT_MAX;
+      for (int w = 0; w < 8; ++w) {
+        if (better(wbest[w], wbi[w], b0, i0)) { b0 = wbest[w]; i0 = wbi[w]; }
+        s0 += wsum[w];
+      }
+      double* sl = p.slots + ((size_t)slot * G + g) * 3;
+      sl[0] = b0; sl[1] = (double)i0; sl[2] = s0;
+    }
+  };
+  publish(0);
+  grid_sync(p.bar);
+
+  int c = 0;
+  for (; c < p.b_req; ++c) {
+    // global argmax + total remaining sketch mass (fixed order -> identical in every CTA)
+    if (tid == 0) {
+      double b0 = -1.0, s0 = 0.0;
+      int i0 = INT_MAX;
+      const double* sl = p.slots + (size_t)(c & 1) * G * 3;
+      for (int h = 0; h < G; ++h) {
+        if (better(sl[3 * h], (int)sl[3 * h + 1], b0, i0)) { b0 = sl[3 * h]; i0 = (int)sl[3 * h + 1]; }
+        s0 += sl[3 * h + 2];
+      }
+      const double est = c < ell ? s0 / (double)(ell - c) : 0.0;
+      if (g == 0) p.out_est[c] = est;
+      int stop = 0;
+      if (!(b0 > 0.0) || c >= ell) stop = 1;
+      else if (c >= p.b_min && (c % 8) == 0 && est <= p.stop_fro2) stop = 1;
+      sh_stop = stop;
+      sh_piv = i0;
+    }
+    __syncthreads();
+    if (sh_stop) break;
+    const int piv = sh_piv;
+    // Householder vector of the pivot column (rows c..ell-1), computed redundantly per CTA
+    if (warp == 0) {
+      double s = 0.0;
+      for (int i = c + 1 + lane; i < ell; i += 32) {
+        const double y = p.Ys[i + (int64_t)piv * p.ldy];
+        v[i] = y;
+        s += y * y;
+      }
+      s = warp_sum(s);
+      const double alpha = p.Ys[c + (int64_t)piv * p.ldy];
+      double tau = 0.0, scal = 0.0, beta = alpha;
+      if (s > 0.0) {
+        beta = -copysign(sqrt(alpha * alpha + s), alpha);
+        tau = (beta - alpha) / beta;
+        scal = 1.0 / (alpha - beta);
+      }
+      for (int i = c + 1 + lane; i < ell; i += 32) v[i] *= scal;
+      if (lane == 0) {
+        v[c] = 1.0;
+        sh_tau = tau;
+        if (g == 0) { p.piv[c] = piv; p.rdiag[c] = fabs(beta); }
+      }
+    }
+    __syncthreads();
+    const double tau = sh_tau;
+    best = -1.0; sum = 0.0; bi = INT_MAX;
+    for (int64_t q = c0 + warp; q < c1; q += 8) {
+      if (q == piv) {
+        if (lane == 0) p.nrm[q] = -1.0;
+        continue;
+      }
+      if (p.nrm[q] < 0.0) continue;  // chosen earlier
+      double* col = p.Ys + q * p.ldy;
+      double w = 0.0;
+      for (int i = c + lane; i < ell; i += 32) w += v[i] * col[i];
+      w = warp_sum(w) * tau;
+      double s = 0.0;
+      for (int i = c + lane; i < ell; i += 32) {
+        const double y = col[i] - w * v[i];
+        col[i] = y;
+        if (i > c) s += y * y;
+      }
+      s = warp_sum(s);
+      if (lane == 0) p.nrm[q] = s;
+      if (better(s, (int)q, best, bi)) { best = s; bi = (int)q; }
+      sum += s;
+    }
+    __syncthreads();
+    publish((c + 1) & 1);
+    grid_sync(p.bar);
+  }
+  if (g == 0 && tid == 0) {
+    // LAPACK-style swap list: swaps[i] = current position of the i-th pivot when it is
+    // exchanged with position i.
+    int pos[kBlockMax];
+    for (int i = 0; i < c; ++i) pos[i] = p.piv[i];
+    for (int i = 0; i < c; ++i) {
+      const int src = pos[i];
+      p.swaps[i] = src;
+      if (src != i)
+        for (int t = i + 1; t < c; ++t)
+          if (pos[t] == i) pos[t] = src;
+    }
+    *p.out_b = c;
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// permute: apply the swap list to A (all m rows), Y (ℓ rows) and perm (one row).
+// ------------------------------------------------------------------------------------------
+__global__ void permute_kernel(double* __restrict__ A, int64_t lda, int64_t m, double* __restrict__ Y,
+                               int64_t ldy, int ell, int64_t* __restrict__ perm, int64_t j,
+                               const int* __restrict__ swaps, const int* __restrict__ bptr) {
+  __shared__ int sw[kBlockMax];
+  const int b = *bptr;
+  for (int i = threadIdx.x; i < b; i += blockDim.x) sw[i] = swaps[i];
+  __syncthreads();
+  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r < m) {
+    double* row = A + r + j * lda;
+    for (int i = 0; i < b; ++i) {
+      const int s = sw[i];
+      if (s != i) {
+        const double t = row[(int64_t)i * lda];
+        row[(int64_t)i * lda] = row[(int64_t)s * lda];
+        row[(int64_t)s * lda] = t;
+      }
+    }
+  } else if (r < m + ell) {
+    double* row = Y + (r - m) + j * ldy;
+    for (int i = 0; i < b; ++i) {
+      const int s = sw[i];
+      if (s != i) {
+        const double t = row[(int64_t)i * ldy];
+        row[(int64_t)i * ldy] = row[(int64_t)s * ldy];
+        row[(int64_t)s * ldy] = t;
+      }
+    }
+  } else if (r == m + ell) {
+    int64_t* row = perm + j;
+    for (int i = 0; i < b; ++i) {
+      const int s = sw[i];
+      if (s != i) {
+        const int64_t t = row[i];
+        row[i] = row[s];
+        row[s] = t;
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// panel_qr: Householder QR of the mp x b panel at P (column-major, ld).
+// ------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) panel_qr_kernel(PanelParams p) {
+  extern __shared__ double psm[];  // vs[chunk] | ws[b]
+  const int G = gridDim.x, g = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int b = p.b;
+  const int64_t chunk = p.chunk;
+  const int64_t r0 = g * chunk, r1 = min(p.mp, r0 + chunk);
+  double* vs = psm;
+  double* ws = psm + chunk;
+  __shared__ double sh[4];
+  double* P = p.P;
+  const int64_t ld = p.ld;
+
+  // column 0 partial norm (rows > 0)
+  if (warp == 0) {
+    double s = 0.0;
+    for (int64_t i = max(r0, (int64_t)1) + lane; i < r1; i += 32) {
+      const double x = P[i];
+      s += x * x;
+    }
+    s = warp_sum(s);
+    if (lane == 0) p.nslot[g] = s;
+  }
+  grid_sync(p.bar);
+
+  for (int c = 0; c < b; ++c) {
+    if (tid == 0) {
+      double s = 0.0;
+      for (int h = 0; h < G; ++h) s += p.nslot[h];
+      const double alpha = P[c + (int64_t)c * ld];
+      double tau = 0.0, scal = 0.0, beta = alpha;
+      if (s > 0.0) {
+        beta = -copysign(sqrt(alpha * alpha + s), alpha);
+        tau = (beta - alpha) / beta;
+        scal = 1.0 / (alpha - beta);
+      }
+      sh[0] = tau; sh[1] = scal; sh[2] = beta;
+    }
+    __syncthreads();
+    const double tau = sh[0], scal = sh[1];
+    double* colc = P + (int64_t)c * ld;
+    for (int64_t i = r0 + tid; i < r1; i += 256) {
+      double vi = 0.0;
+      if (i > c) {
+        vi = colc[i] * scal;
+        colc[i] = vi;
+      } else if (i == c) {
+        vi = 1.0;
+      }
+      vs[i - r0] = vi;
+    }
+    __syncthreads();
+    const int64_t lo = max(r0, (int64_t)c);
+    // partial w_q = sum_i v_i P[i, q]  (q > c)
+    for (int q = c + 1 + warp; q < b; q += 8) {
+      const double* colq = P + (int64_t)q * ld;
+      double s = 0.0;
+      for (int64_t i = lo + lane; i < r1; i += 32) s += vs[i - r0] * colq[i];
+      s = warp_sum(s);
+      if (lane == 0) p.wslot[(size_t)g * b + q] = s;
+    }
+    grid_sync(p.bar);
+    for (int q = c + 1 + tid; q < b; q += 256) {
+      double s = 0.0;
+      for (int h = 0; h < G; ++h) s += p.wslot[(size_t)h * b + q];
+      ws[q] = s * tau;
+    }
+    __syncthreads();
+    for (int q = c + 1 + warp; q < b; q += 8) {
+      double* colq = P + (int64_t)q * ld;
+      const double wq = ws[q];
+      double s = 0.0;
+      for (int64_t i = lo + lane; i < r1; i += 32) {
+        const double x = colq[i] - vs[i - r0] * wq;
+        colq[i] = x;
+        if (q == c + 1 && i > c + 1) s += x * x;
+      }
+      if (q == c + 1) {
+        s = warp_sum(s);
+        if (lane == 0) p.nslot[g] = s;
+      }
+    }
+    if (c + 1 >= b && tid == 0) p.nslot[g] = 0.0;
+    if (c >= r0 && c < r1 && tid == 0) colc[c] = sh[2];
+    if (g == 0 && tid == 0) p.tau[c] = tau;
+    grid_sync(p.bar);
+  }
+  // explicit V (unit diagonal, zeros above)
+  for (int q = warp; q < b; q += 8) {
+    const double* colq = P + (int64_t)q * ld;
+    double* vq = p.V + (int64_t)q * p.ldv;
+    for (int64_t i = r0 + lane; i < r1; i += 32) vq[i] = i > q ? colq[i] : (i == q ? 1.0 : 0.0);
+  }
+}
+
+// T of the compact-WY form from S = VᵀV and τ (LAPACK dlarft, forward/columnwise).
+__global__ void build_T_kernel(const double* __restrict__ S, int64_t lds, const double* __restrict__ tau,
+                               int b, double* __restrict__ T, int64_t ldt) {
+  extern __shared__ double Ts[];  // b x b, ld b
+  const int t = threadIdx.x;
+  for (int e = t; e < b * b; e += blockDim.x) Ts[e] = 0.0;
+  __syncthreads();
+  for (int c = 0; c < b; ++c) {
+    const double tc = tau[c];
+    if (t < c) {
+      double s = 0.0;
+      for (int k = t; k < c; ++k) s += Ts[t + k * b] * S[k + (int64_t)c * lds];
+      Ts[t + c * b] = -tc * s;
+    } else if (t == c) {
+      Ts[c + c * b] = tc;
+    }
+    __syncthreads();
+  }
+  for (int e = t; e < b * b; e += blockDim.x) T[(e % b) + (int64_t)(e / b) * ldt] = Ts[e];
+}
+
+// Z (ell x b) = Y1 R11^{-1}: row-wise forward substitution, one thread per sketch row.
+__global__ void sketch_trsm_kernel(const double* __restrict__ Y1, int64_t ldy, int ell,
+                                   const double* __restrict__ R, int64_t ldr, int b,
+                                   double* __restrict__ Z, int64_t ldz) {
+  extern __shared__ double Rs[];  // b x b upper
+  for (int e = threadIdx.x; e < b * b; e += blockDim.x) {
+    const int i = e % b, c = e / b;
+    Rs[e] = i <= c ? R[i + (int64_t)c * ldr] : 0.0;
+  }
+  __syncthreads();
+  const int t = threadIdx.x;
+  if (t >= ell) return;
+  for (int c = 0; c < b; ++c) {
+    double s = Y1[t + (int64_t)c * ldy];
+    for (int i = 0; i < c; ++i) s -= Z[t + (int64_t)i * ldz] * Rs[i + c * b];
+    const double d = Rs[c + c * b];
+    Z[t + (int64_t)c * ldz] = d != 0.0 ? s / d : 0.0;
+  }
+}
+
+// σ₁ lower bound: power iteration on R_b = rows 0..b-1 of the factor (upper trapezoidal; the
+// strictly-lower part of the first b columns holds V and is masked).
+__global__ void __launch_bounds__(256) power_sigma1_kernel(PowerParams p) {
+  const int G = gridDim.x, g = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int b = p.b;
+  const int64_t cpc = ceil_div(p.n, G);
+  const int64_t c0 = g * cpc, c1 = min(p.n, c0 + cpc);
+  __shared__ double x[kBlockMax], acc[8][kBlockMax];
+  __shared__ double ysum[8];
+  __shared__ double sh_norm;
+  double best = 0.0;
+  for (int it = 0; it <= p.iters; ++it) {
+    // x from previous partials (it == 0: ones)
+    if (tid < b) {
+      double s = 0.0;
+      if (it == 0) s = 1.0;
+      else
+        for (int h = 0; h < G; ++h) s += p.slots[(size_t)((it - 1) & 1) * G * (b + 1) + (size_t)h * (b + 1) + tid];
+      x[tid] = s;
+    }
+    if (tid == 0 && it > 0) {
+      double s = 0.0;
+      for (int h = 0; h < G; ++h) s += p.slots[(size_t)((it - 1) & 1) * G * (b + 1) + (size_t)h * (b + 1) + b];
+      best = fmax(best, sqrt(s));  // ||R^T x_hat|| of the previous iterate
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double s = 0.0;
+      for (int i = 0; i < b; ++i) s += x[i] * x[i];
+      sh_norm = s > 0.0 ? 1.0 / sqrt(s) : 0.0;
+    }
+    __syncthreads();
+    if (tid < b) x[tid] *= sh_norm;
+    for (int i = tid; i < 8 * kBlockMax; i += 256) (&acc[0][0])[i] = 0.0;
+    __syncthreads();
+    if (it == p.iters) break;
+    double yy = 0.0;
+    for (int64_t c = c0 + warp; c < c1; c += 8) {
+      const double* col = p.R + c * p.ld;
+      const int rmax = c < b ? (int)c + 1 : b;
+      double s = 0.0;
+      for (int i = lane; i < rmax; i += 32) s += col[i] * x[i];
+      s = warp_sum(s);
+      yy += s * s;
+      for (int i = lane; i < rmax; i += 32) acc[warp][i] += col[i] * s;
+    }
+    if (lane == 0) ysum[warp] = yy;
+    __syncthreads();
+    double* sl = p.slots + (size_t)(it & 1) * G * (b + 1) + (size_t)g * (b + 1);
+    if (tid < b) {
+      double s = 0.0;
+      for (int w = 0; w < 8; ++w) s += acc[w][tid];
+      sl[tid] = s;
+    }
+    if (tid == 0) {
+      double s = 0.0;
+      for (int w = 0; w < 8; ++w) s += ysum[w];
+      sl[b] = s;
+    }
+    grid_sync(p.bar);
+  }
+  if (g == 0 && tid == 0) *p.out = best;
+}
+
+__global__ void sum_kernel(const double* __restrict__ parts, int64_t n, double* __restrict__ out) {
+  __shared__ double red[32];
+  double s = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s += parts[i];
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) *out = s;
+}
+
+// B (n x k) = upper-trapezoidal rows 0..k-1 of A (m x n), transposed; zero below the diagonal.
+__global__ void transpose_upper_kernel(const double* __restrict__ A, int64_t lda, int64_t k,
+                                       int64_t n, double* __restrict__ B, int64_t ldb) {
+  __shared__ double tile[32][33];
+  const int64_t i0 = (int64_t)blockIdx.y * 32, c0 = (int64_t)blockIdx.x * 32;
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int64_t c = c0 + r, i = i0 + threadIdx.x;
+    tile[r][threadIdx.x] = (i < k && c < n && c >= i) ? A[i + c * lda] : 0.0;
+  }
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int64_t i = i0 + r, c = c0 + threadIdx.x;
+    if (i < k && c < n) B[c + i * ldb] = tile[threadIdx.x][r];
+  }
+}
+
+// C (k x k) = upper triangle of B[0:k, 0:k].
+__global__ void copy_upper_kernel(const double* __restrict__ B, int64_t ldb, int64_t k,
+                                  double* __restrict__ C, int64_t ldc) {
+  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= k * k) return;
+  const int64_t i = idx % k, c = idx / k;
+  C[i + c * ldc] = i <= c ? B[i + c * ldb] : 0.0;
+}
+
+}  // namespace hb
+
+namespace hb {
+__global__ void iota_kernel(int64_t* __restrict__ p, int64_t n) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) p[i] = i;
+}
+__global__ void nonfinite_kernel(const double* __restrict__ A, int64_t m, int64_t n, int64_t ld,
+                                 unsigned int* flags) {
+  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= m * n) return;
+  const int64_t i = idx % m, c = idx / m;
+  if (!isfinite(A[i + c * ld])) atomicOr(flags, 2u);
+}
+}  // namespace hb

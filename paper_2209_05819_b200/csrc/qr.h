@@ -1,0 +1,100 @@
+// Parameter blocks of the cooperative QR / SVD kernels (internal).
+#pragma once
+
+#include "common.cuh"
+
+namespace hb {
+
+struct SketchParams {
+  const double* Y;  // ℓ x n_tr sketch of the trailing columns (ld = ldy)
+  double* Ys;       // scratch copy, same shape
+  double* nrm;      // n_tr scratch column norms (-1 = chosen)
+  int ell;
+  int64_t ldy;
+  int64_t n_tr;
+  int b_req;        // pivots wanted (<= kBlockMax)
+  int b_min;        // fewest pivots before the early stop may fire
+  double stop_fro2; // early stop when the sketch estimate of ||A22||_F^2 <= this
+  double* slots;    // [2][G][3]
+  int* piv;         // [b_req] pivot column (relative to the trailing start)
+  int* swaps;       // [b_req] LAPACK-style swap targets
+  double* rdiag;    // [b_req] |R_cc| of the sketch
+  double* out_est;  // [b_req + 1] sketch estimate of ||A22||_F^2 before step c
+  int* out_b;       // pivots chosen
+  GridBarrier bar;
+};
+
+struct PanelParams {
+  double* P;  // panel (mp x b), column-major
+  int64_t ld;
+  int64_t mp;
+  int b;
+  int64_t chunk;   // rows per CTA
+  double* tau;     // [b]
+  double* V;       // explicit V (mp x b)
+  int64_t ldv;
+  double* nslot;   // [G]
+  double* wslot;   // [G][b]
+  GridBarrier bar;
+};
+
+struct PowerParams {
+  const double* R;  // rows 0..b-1 of the factor
+  int64_t ld;
+  int b;
+  int64_t n;
+  int iters;
+  double* slots;  // [2][G][b+1]
+  double* out;
+  GridBarrier bar;
+};
+
+struct BidiagParams {
+  double* M;  // k x k, column-major (destroyed)
+  int64_t ld;
+  int64_t k;
+  double* d;      // [k]   diagonal of the upper bidiagonal
+  double* e;      // [k]   superdiagonal (k-1 used)
+  double* wslot;  // [G][k] column partials
+  double* w;      // [k]
+  double* v;      // [k]
+  double* nslot;  // [G]
+  double* scal;   // [4] broadcast scalars
+  GridBarrier bar;
+};
+
+__global__ void sketch_cpqr_kernel(SketchParams p);
+__global__ void permute_kernel(double* A, int64_t lda, int64_t m, double* Y, int64_t ldy, int ell,
+                               int64_t* perm, int64_t j, const int* swaps, const int* bptr);
+__global__ void panel_qr_kernel(PanelParams p);
+__global__ void build_T_kernel(const double* S, int64_t lds, const double* tau, int b, double* T,
+                               int64_t ldt);
+__global__ void sketch_trsm_kernel(const double* Y1, int64_t ldy, int ell, const double* R,
+                                   int64_t ldr, int b, double* Z, int64_t ldz);
+__global__ void power_sigma1_kernel(PowerParams p);
+__global__ void sum_kernel(const double* parts, int64_t n, double* out);
+__global__ void transpose_upper_kernel(const double* A, int64_t lda, int64_t k, int64_t n, double* B,
+                                       int64_t ldb);
+__global__ void copy_upper_kernel(const double* B, int64_t ldb, int64_t k, double* C, int64_t ldc);
+__global__ void bidiag_kernel(BidiagParams p);
+
+// Bisection on the upper bidiagonal (d, e): singular-value queries.
+struct SigmaQuery {
+  double tol;     // relative tolerance
+  double delta;   // residual bound δ for rank_hi
+};
+struct SigmaAnswer {
+  double sigma1, sigma_p, sigma_p1;
+  int rank_lo, rank_hi;
+};
+__global__ void sigma_queries_kernel(const double* d, const double* e, int64_t k,
+                                     const SigmaQuery* q, int nq, SigmaAnswer* out);
+__global__ void sigma_all_kernel(const double* d, const double* e, int64_t k, double sigma_max,
+                                 double* out);
+
+}  // namespace hb
+
+namespace hb {
+__global__ void iota_kernel(int64_t* p, int64_t n);
+__global__ void nonfinite_kernel(const double* A, int64_t m, int64_t n, int64_t ld, unsigned int* flags);
+}  // namespace hb

@@ -1,0 +1,359 @@
+// Host driver of k3: sketch-pivoted blocked QR + certification (one problem, one stream).
+//
+// Replaces SPEC `epsilon_rank` — the count of σ_k > tol·σ₁ of a dense block —
+// with a factorisation whose cost scales with the ε-rank p instead of N³:
+//   1. Y = Ω A (ℓ = 128 Gaussian rows).
+//   2. per block of b <= 120 columns: sketch CPQR picks pivots -> swap -> Householder panel ->
+//      T -> A2 ← (I − V Tᵀ Vᵀ) A2 with the exact ||A22||_F² in the GEMM epilogue -> Y downdate.
+//   3. stop when δ = ||A22||_F <= η·tol·σ̂₁ (σ̂₁: power-iteration lower bound on σ₁).
+//   4. certify: σ(R_k) from QR(R_kᵀ) -> bidiagonal -> bisection; then
+//        rank_lo = #σ(R_k) > thr <= true rank <= rank_hi = #σ(R_k) > sqrt(thr² − δ²)
+//      (σ_i(R_k) <= σ_i(A) <= sqrt(σ_i(R_k)² + δ²) by Weyl, since AᵀA = R_kᵀR_k + EᵀE, ||E|| = δ).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "context.h"
+
+namespace hb {
+
+namespace {
+
+template <typename P>
+void coop(void (*kern)(P), int grid, size_t smem, cudaStream_t st, P prm) {
+  void* args[] = {&prm};
+  if (smem > 48 * 1024)
+    HB_CUDA(cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem));
+  HB_CUDA(cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(256), args, smem, st));
+}
+
+int clampi(int64_t v, int lo, int hi) { return (int)std::max<int64_t>(lo, std::min<int64_t>(hi, v)); }
+
+void sync_to_host(hb_context* c, const void* dsrc, void* hdst, size_t bytes) {
+  HB_CUDA(cudaMemcpyAsync(c->pinned, dsrc, bytes, cudaMemcpyDeviceToHost, c->stream));
+  HB_CUDA(cudaStreamSynchronize(c->stream));
+  std::memcpy(hdst, c->pinned, bytes);
+}
+
+GridBarrier barrier(hb_context* c) { return GridBarrier{c->bar, c->bar + 1}; }
+
+struct Gemm {
+  hb_context* c;
+  void operator()(const GemmArgs& g) {
+    double* sk = ws<double>(c, B_SPLITK, kSplitKElems);
+    launch_dgemm(g, sk, kSplitKElems, c->num_sms, c->stream);
+  }
+  static constexpr int64_t kSplitKElems = 8ll << 20;
+};
+
+// Householder panel + compact-WY T.  Panel mp x b at P (ld); V (ld ldv) and T (ld b) out.
+void panel_and_T(hb_context* c, double* P, int64_t ld, int64_t mp, int b, double* V, int64_t ldv,
+                 double* tau, double* T) {
+  const int G = clampi(ceil_div(mp, 256), 1, c->num_sms);
+  PanelParams pp{};
+  pp.P = P; pp.ld = ld; pp.mp = mp; pp.b = b;
+  pp.chunk = ceil_div(mp, G);
+  pp.tau = tau; pp.V = V; pp.ldv = ldv;
+  double* slots = ws<double>(c, B_SLOTS, (size_t)c->num_sms * (kBlockMax + 1) * 2 + 64);
+  pp.nslot = slots;
+  pp.wslot = slots + c->num_sms;
+  pp.bar = barrier(c);
+  const size_t smem = (size_t)(pp.chunk + b) * sizeof(double);
+  HB_REQUIRE(smem <= 200 * 1024, HB_ECAP, "panel: too many rows per CTA");
+  coop(panel_qr_kernel, G, smem, c->stream, pp);
+  // S = VᵀV, T from (S, τ)
+  double* S = ws<double>(c, B_S, kBlockMax * kBlockMax);
+  GemmArgs g{};
+  g.M = b; g.N = b; g.K = mp; g.alpha = 1.0; g.A = V; g.lda = ldv; g.transA = true;
+  g.B = V; g.ldb = ldv; g.beta = 0.0; g.C = S; g.ldc = b;
+  Gemm{c}(g);
+  const size_t tsm = (size_t)b * b * sizeof(double);
+  if (tsm > 48 * 1024)
+    HB_CUDA(cudaFuncSetAttribute((const void*)build_T_kernel,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm));
+  build_T_kernel<<<1, 128, tsm, c->stream>>>(S, b, tau, b, T, b);
+  HB_LAUNCH_CHECK();
+}
+
+// A2 (mp x n2, ld) ← (I − V Tᵀ Vᵀ) A2; if fro != nullptr the exact sum of squares of rows >= b of
+// the updated A2 is accumulated into *fro_dev (device scalar).
+void apply_block_reflector(hb_context* c, const double* V, int64_t ldv, const double* T, int b,
+                           double* A2, int64_t ld, int64_t mp, int64_t n2, double* fro_dev) {
+  if (n2 <= 0) return;
+  double* W = ws<double>(c, B_W, (size_t)kBlockMax * n2);
+  double* W2 = ws<double>(c, B_W2, (size_t)kBlockMax * n2);
+  Gemm gemm{c};
+  GemmArgs g{};
+  g.M = b; g.N = n2; g.K = mp; g.alpha = 1.0; g.A = V; g.lda = ldv; g.transA = true;
+  g.B = A2; g.ldb = ld; g.beta = 0.0; g.C = W; g.ldc = b;
+  gemm(g);
+  GemmArgs g2{};
+  g2.M = b; g2.N = n2; g2.K = b; g2.alpha = 1.0; g2.A = T; g2.lda = b; g2.transA = true;
+  g2.B = W; g2.ldb = b; g2.beta = 0.0; g2.C = W2; g2.ldc = b;
+  gemm(g2);
+  GemmArgs g3{};
+  g3.M = mp; g3.N = n2; g3.K = b; g3.alpha = -1.0; g3.A = V; g3.lda = ldv; g3.transA = false;
+  g3.B = W2; g3.ldb = b; g3.beta = 1.0; g3.C = A2; g3.ldc = ld;
+  double* parts = nullptr;
+  int64_t cnt = 0;
+  if (fro_dev) {
+    cnt = gemm_fro_count(mp, n2);
+    parts = ws<double>(c, B_FRO, (size_t)cnt);
+    g3.fro_partials = parts;
+    g3.fro_row0 = b;
+  }
+  gemm(g3);
+  if (fro_dev) {
+    sum_kernel<<<1, 1024, 0, c->stream>>>(parts, cnt, fro_dev);
+    HB_LAUNCH_CHECK();
+  }
+}
+
+void sketch(hb_context* c, const double* A, int64_t lda, int64_t m, int64_t n, double* Y,
+            uint64_t seed) {
+  double* Om = ws<double>(c, B_OMEGA, (size_t)kSketchRows * std::max<int64_t>(m, 1));
+  launch_gaussian(Om, kSketchRows, m, kSketchRows, seed, c->stream);
+  GemmArgs g{};
+  g.M = kSketchRows; g.N = n; g.K = m; g.alpha = 1.0; g.A = Om; g.lda = kSketchRows;
+  g.transA = false; g.B = A; g.ldb = lda; g.beta = 0.0; g.C = Y; g.ldc = kSketchRows;
+  Gemm{c}(g);
+}
+
+}  // namespace
+
+void rank_matrix_inplace(hb_context* c, double* A, int64_t m, int64_t n, int64_t lda,
+                         const double* tols, int ntol, hb_rank_result* out, float* fact_ms,
+                         float* cert_ms) {
+  cudaStream_t st = c->stream;
+  const int ell = kSketchRows;
+  const int64_t kmax = std::min(m, n);
+  double tol_min = tols[0];
+  for (int t = 1; t < ntol; ++t) tol_min = std::min(tol_min, tols[t]);
+
+  HB_CUDA(cudaEventRecord(c->ev[1], st));
+  double* Y = ws<double>(c, B_YSK, (size_t)ell * n);
+  double* Ys = ws<double>(c, B_YS, (size_t)ell * n);
+  double* nrm = ws<double>(c, B_NRM, (size_t)n);
+  const int64_t ldv = round_up(std::max(m, n), 8);
+  double* V = ws<double>(c, B_V, (size_t)ldv * kBlockMax);
+  double* T = ws<double>(c, B_T, kBlockMax * kBlockMax);
+  double* Z = ws<double>(c, B_Z, (size_t)ell * kBlockMax);
+  double* tau = ws<double>(c, B_TAU, kBlockMax);
+  int* piv = ws<int>(c, B_PIV, kBlockMax);
+  int* swaps = ws<int>(c, B_SWAPS, kBlockMax);
+  double* rdiag = ws<double>(c, B_RDIAG, kBlockMax);
+  double* est = ws<double>(c, B_EST, kBlockMax + 1);
+  int* beff = ws<int>(c, B_BEFF, 4);
+  int64_t* perm = ws<int64_t>(c, B_PERM, (size_t)n);
+  double* scal = ws<double>(c, B_FROSUM, 8);  // [0] fro², [1] σ̂₁
+  double* sk_slots = ws<double>(c, B_SCAL, (size_t)c->num_sms * 6 + 16);
+  iota_kernel<<<(unsigned)ceil_div(std::max<int64_t>(n, 1), 256), 256, 0, c->stream>>>(perm, n);
+  HB_LAUNCH_CHECK();
+
+  uint64_t sketch_seed = 0x243F6A8885A308D3ull;
+  if (kmax > 0) sketch(c, A, lda, m, n, Y, sketch_seed);
+
+  int64_t j = 0;
+  int b = std::min(32, c->block_max);
+  double sigma1_est = 0.0, delta = 0.0, fro_at_sketch = INFINITY;
+  bool first = true;
+  int zero_retries = 0;
+  while (j < kmax) {
+    const int b_req = (int)std::min<int64_t>({(int64_t)b, kmax - j, (int64_t)kBlockMax});
+    const int64_t n_tr = n - j, mp = m - j;
+    SketchParams sp{};
+    sp.Y = Y + j * ell; sp.Ys = Ys; sp.nrm = nrm; sp.ell = ell; sp.ldy = ell; sp.n_tr = n_tr;
+    sp.b_req = b_req; sp.b_min = std::min(8, b_req);
+    const double stop_res = 0.5 * c->eta * tol_min * sigma1_est;
+    sp.stop_fro2 = sigma1_est > 0.0 ? stop_res * stop_res : -1.0;
+    sp.slots = sk_slots; sp.piv = piv; sp.swaps = swaps; sp.rdiag = rdiag; sp.out_est = est;
+    sp.out_b = beff; sp.bar = barrier(c);
+    coop(sketch_cpqr_kernel, clampi(ceil_div(n_tr, 128), 1, c->num_sms), 0, st, sp);
+    int bh = 0;
+    sync_to_host(c, beff, &bh, sizeof(int));
+    if (bh == 0) {
+      // the sketch of the trailing matrix vanished: re-sketch once, else the trailing block is 0
+      if (zero_retries++ < 1) {
+        sketch_seed = splitmix64(sketch_seed);
+        double* Om = ws<double>(c, B_OMEGA, (size_t)ell * std::max<int64_t>(mp, 1));
+        launch_gaussian(Om, ell, mp, ell, sketch_seed, st);
+        GemmArgs g{};
+        g.M = ell; g.N = n_tr; g.K = mp; g.alpha = 1.0; g.A = Om; g.lda = ell;
+        g.B = A + j + j * lda; g.ldb = lda; g.beta = 0.0; g.C = Y + j * ell; g.ldc = ell;
+        Gemm{c}(g);
+        continue;
+      }
+      break;
+    }
+    zero_retries = 0;
+    permute_kernel<<<(unsigned)ceil_div(m + ell + 1, 256), 256, 0, st>>>(A, lda, m, Y, ell, ell,
+                                                                           perm, j, swaps, beff);
+    HB_LAUNCH_CHECK();
+    double* P = A + j + j * lda;
+    panel_and_T(c, P, lda, mp, bh, V, ldv, tau, T);
+    const int64_t n2 = n - j - bh;
+    if (n2 > 0 && mp > bh) {
+      apply_block_reflector(c, V, ldv, T, bh, A + j + (j + bh) * lda, lda, mp, n2, scal);
+    } else {
+      if (n2 > 0) apply_block_reflector(c, V, ldv, T, bh, A + j + (j + bh) * lda, lda, mp, n2, nullptr);
+      HB_CUDA(cudaMemsetAsync(scal, 0, sizeof(double), st));
+    }
+    if (first) {
+      PowerParams pw{};
+      pw.R = A; pw.ld = lda; pw.b = bh; pw.n = n; pw.iters = 40;
+      pw.slots = ws<double>(c, B_SIG1, (size_t)2 * c->num_sms * (kBlockMax + 1));
+      pw.out = scal + 1; pw.bar = barrier(c);
+      coop(power_sigma1_kernel, clampi(ceil_div(n, 256), 1, c->num_sms), 0, st, pw);
+    }
+    if (n2 > 0) {
+      const size_t rsm = (size_t)bh * bh * sizeof(double);
+      if (rsm > 48 * 1024)
+        HB_CUDA(cudaFuncSetAttribute((const void*)sketch_trsm_kernel,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm));
+      sketch_trsm_kernel<<<1, ell, rsm, st>>>(Y + j * ell, ell, ell, P, lda, bh, Z, ell);
+      HB_LAUNCH_CHECK();
+      GemmArgs g{};
+      g.M = ell; g.N = n2; g.K = bh; g.alpha = -1.0; g.A = Z; g.lda = ell;
+      g.B = A + j + (j + bh) * lda; g.ldb = lda; g.beta = 1.0; g.C = Y + (j + bh) * ell; g.ldc = ell;
+      Gemm{c}(g);
+    }
+    j += bh;
+    double hs[2];
+    sync_to_host(c, scal, hs, sizeof(hs));
+    delta = std::sqrt(std::max(hs[0], 0.0));
+    if (first) {
+      sigma1_est = hs[1];
+      first = false;
+    }
+    if (j >= kmax) break;
+    if (delta <= c->eta * tol_min * sigma1_est) break;
+    if (!(fro_at_sketch < INFINITY)) fro_at_sketch = delta;
+    if (delta < 1e-8 * fro_at_sketch) {
+      // the downdated sketch has lost ~8 digits to cancellation: draw a fresh one
+      sketch_seed = splitmix64(sketch_seed);
+      const int64_t mr = m - j;
+      double* Om = ws<double>(c, B_OMEGA, (size_t)ell * std::max<int64_t>(mr, 1));
+      launch_gaussian(Om, ell, mr, ell, sketch_seed, st);
+      GemmArgs g{};
+      g.M = ell; g.N = n - j; g.K = mr; g.alpha = 1.0; g.A = Om; g.lda = ell;
+      g.B = A + j + j * lda; g.ldb = lda; g.beta = 0.0; g.C = Y + j * ell; g.ldc = ell;
+      Gemm{c}(g);
+      fro_at_sketch = delta;
+    }
+    b = std::min(2 * b, c->block_max);
+  }
+  if (j >= kmax) delta = 0.0;
+  const int64_t k = j;
+  HB_CUDA(cudaEventRecord(c->ev[2], st));
+
+  // ---- certification: σ(R_k) ------------------------------------------------------------
+  SigmaQuery hq[HB_MAX_TOLS];
+  for (int t = 0; t < ntol; ++t) hq[t] = SigmaQuery{tols[t], delta};
+  SigmaAnswer ans[HB_MAX_TOLS];
+  std::memset(ans, 0, sizeof(ans));
+  if (k > 0) {
+    const int64_t ldb = round_up(n, 8);
+    double* Bc = ws<double>(c, B_CERT_B, (size_t)ldb * k);
+    dim3 tb(32, 8), tg((unsigned)ceil_div(n, 32), (unsigned)ceil_div(k, 32));
+    transpose_upper_kernel<<<tg, tb, 0, st>>>(A, lda, k, n, Bc, ldb);
+    HB_LAUNCH_CHECK();
+    const int bq_max = kBlockMax;
+    for (int64_t jj = 0; jj < k; jj += bq_max) {
+      const int bq = (int)std::min<int64_t>(bq_max, k - jj);
+      double* P = Bc + jj + jj * ldb;
+      panel_and_T(c, P, ldb, n - jj, bq, V, ldv, tau, T);
+      if (jj + bq < k)
+        apply_block_reflector(c, V, ldv, T, bq, Bc + jj + (jj + bq) * ldb, ldb, n - jj,
+                              k - jj - bq, nullptr);
+    }
+    const int64_t ldm = round_up(k, 8);
+    double* Mk = ws<double>(c, B_CERT_M, (size_t)ldm * k);
+    copy_upper_kernel<<<(unsigned)ceil_div(k * k, 256), 256, 0, st>>>(Bc, ldb, k, Mk, ldm);
+    HB_LAUNCH_CHECK();
+    double* d = ws<double>(c, B_D, (size_t)k + 1);
+    double* e = ws<double>(c, B_E, (size_t)k + 1);
+    HB_CUDA(cudaMemsetAsync(e, 0, sizeof(double) * (k + 1), st));
+    const int64_t nb = ceil_div(k, 32);
+    const int G = clampi(nb, 1, c->num_sms);
+    const int64_t nown = ceil_div(nb, G);
+    BidiagParams bp{};
+    bp.M = Mk; bp.ld = ldm; bp.k = k; bp.d = d; bp.e = e;
+    bp.wslot = ws<double>(c, B_BW, (size_t)G * k);
+    bp.w = ws<double>(c, B_BV, (size_t)2 * k + 8);
+    bp.v = bp.w + k + 4;
+    bp.nslot = ws<double>(c, B_SLOTS, (size_t)c->num_sms * (kBlockMax + 1) * 2 + 64);
+    bp.scal = scal + 4;
+    bp.bar = barrier(c);
+    const size_t smem = (size_t)nown * 32 * 9 * sizeof(double);
+    HB_REQUIRE(smem <= 200 * 1024, HB_ECAP, "bidiag: k too large");
+    coop(bidiag_kernel, G, smem, st, bp);
+    SigmaQuery* dq = ws<SigmaQuery>(c, B_QUERY, HB_MAX_TOLS);
+    SigmaAnswer* da = ws<SigmaAnswer>(c, B_ANSWER, HB_MAX_TOLS);
+    HB_CUDA(cudaMemcpyAsync(dq, hq, sizeof(SigmaQuery) * ntol, cudaMemcpyHostToDevice, st));
+    sigma_queries_kernel<<<1, 32 * HB_MAX_TOLS, 0, st>>>(d, e, k, dq, ntol, da);
+    HB_LAUNCH_CHECK();
+    sync_to_host(c, da, ans, sizeof(SigmaAnswer) * ntol);
+  }
+  HB_CUDA(cudaEventRecord(c->ev[3], st));
+  HB_CUDA(cudaEventSynchronize(c->ev[3]));
+  float f_ms = 0.f, c_ms = 0.f;
+  HB_CUDA(cudaEventElapsedTime(&f_ms, c->ev[1], c->ev[2]));
+  HB_CUDA(cudaEventElapsedTime(&c_ms, c->ev[2], c->ev[3]));
+  if (fact_ms) *fact_ms = f_ms;
+  if (cert_ms) *cert_ms = c_ms;
+  c->last_k = k;
+  c->last_sigma1 = k > 0 ? ans[0].sigma1 : 0.0;
+  for (int t = 0; t < ntol; ++t) {
+    hb_rank_result& r = out[t];
+    std::memset(&r, 0, sizeof(r));
+    r.rank = ans[t].rank_lo;
+    r.rank_lo = ans[t].rank_lo;
+    r.rank_hi = ans[t].rank_hi;
+    r.k_factored = (int32_t)k;
+    r.sigma1 = ans[t].sigma1;
+    r.sigma_r = ans[t].sigma_p;
+    r.sigma_r1 = ans[t].sigma_p1;
+    const double thr = tols[t] * ans[t].sigma1;
+    double gap = INFINITY;
+    if (thr > 0.0) {
+      if (r.rank > 0) gap = std::min(gap, r.sigma_r / thr - 1.0);
+      if (r.rank < kmax) gap = std::min(gap, 1.0 - r.sigma_r1 / thr);
+    }
+    r.gap = gap;
+    r.resid = delta;
+    r.sec[1] = f_ms * 1e-3;
+    r.sec[2] = c_ms * 1e-3;
+  }
+}
+
+void context_init(hb_context* c, int device) {
+  c->device = device;
+  HB_CUDA(cudaSetDevice(device));
+  HB_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  HB_CUDA(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
+  cudaMemPool_t pool;
+  HB_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+  uint64_t thr = UINT64_MAX;
+  HB_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+  HB_CUDA(cudaMalloc(&c->bar, 4 * sizeof(unsigned int)));
+  HB_CUDA(cudaMemset(c->bar, 0, 4 * sizeof(unsigned int)));
+  HB_CUDA(cudaMallocHost(&c->pinned, 4096));
+  for (auto& e : c->ev) HB_CUDA(cudaEventCreate(&e));
+  c->bufs.resize(B_COUNT);
+}
+
+void context_free(hb_context* c) {
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  for (auto& b : c->bufs)
+    if (b.p) cudaFreeAsync(b.p, c->stream);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  if (c->bar) cudaFree(c->bar);
+  if (c->pinned) cudaFreeHost(c->pinned);
+  for (auto& e : c->ev)
+    if (e) cudaEventDestroy(e);
+  if (c->stream) cudaStreamDestroy(c->stream);
+}
+
+}  // namespace hb

@@ -1,0 +1,259 @@
+// Certification kernels: Golub–Kahan bidiagonalisation of the k x k triangle R' (from the QR of
+// R_kᵀ) and Sturm-count bisection on the Golub–Kahan tridiagonal (TGK) of the bidiagonal.
+//
+// The ε-rank definition needs singular values; the rank
+// test count(σ > tol·σ₁) and the boundary gap only need σ₁, σ_p, σ_{p+1} and two counts, which
+// bisection on the bidiagonal delivers to high relative accuracy without computing the rest.
+//
+// bidiag_kernel (grid-cooperative): rows are dealt to CTAs in 32-row blocks, block-cyclically;
+// a warp processes one column segment of 32 rows at a time (coalesced 256-byte accesses).  Per
+// step i: left reflector u from column i (partial norms -> barrier), wᵀ = uᵀM (partials ->
+// barrier -> distributed reduce -> barrier), rank-1 update, right reflector v from row i (owner
+// CTA -> barrier), z = M v and rank-1 update done row-locally (no reduction across CTAs).
+#include "common.cuh"
+#include "kernels.h"
+#include "qr.h"
+
+namespace hb {
+
+__global__ void __launch_bounds__(256) bidiag_kernel(BidiagParams p) {
+  extern __shared__ double bsm[];
+  const int G = gridDim.x, g = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t k = p.k, ld = p.ld;
+  double* M = p.M;
+  const int64_t nb = ceil_div(k, 32);
+  const int64_t nown = g < nb ? ceil_div(nb - g, G) : 0;  // own blocks: g, g+G, ...
+  double* u = bsm;                      // [nown*32]
+  double* zp = bsm + nown * 32;         // [8][nown*32]
+  __shared__ double sh[4];
+
+  auto own_row = [&](int64_t t) { return (g + t * G) * 32; };
+
+  // partial norm of column 0 (rows > 0)
+  {
+    double s = 0.0;
+    if (warp == 0)
+      for (int64_t t = 0; t < nown; ++t) {
+        const int64_t r = own_row(t) + lane;
+        if (r > 0 && r < k) { const double x = M[r]; s += x * x; }
+      }
+    s = warp_sum(s);
+    if (tid == 0) p.nslot[g] = s;
+  }
+  grid_sync(p.bar);
+
+  for (int64_t i = 0; i < k; ++i) {
+    // ---- left reflector from column i ----
+    if (tid == 0) {
+      double s = 0.0;
+      for (int h = 0; h < G; ++h) s += p.nslot[h];
+      const double alpha = M[i + i * ld];
+      double tau = 0.0, scal = 0.0, beta = alpha;
+      if (s > 0.0) {
+        beta = -copysign(sqrt(alpha * alpha + s), alpha);
+        tau = (beta - alpha) / beta;
+        scal = 1.0 / (alpha - beta);
+      }
+      sh[0] = tau; sh[1] = scal;
+      if (g == 0) p.d[i] = beta;
+    }
+    __syncthreads();
+    const double tau_u = sh[0], scal_u = sh[1];
+    for (int64_t e = tid; e < nown * 32; e += 256) {
+      const int64_t r = own_row(e / 32) + (e % 32);
+      double ur = 0.0;
+      if (r < k) ur = r > i ? M[r + i * ld] * scal_u : (r == i ? 1.0 : 0.0);
+      u[e] = ur;
+    }
+    __syncthreads();
+    const int64_t t0 = i / 32 >= g ? (i / 32 - g + G - 1) / G : 0;  // first own block with rows >= i
+    if (i + 1 < k) {
+      for (int64_t q = i + 1 + warp; q < k; q += 8) {
+        const double* col = M + q * ld;
+        double s = 0.0;
+        for (int64_t t = t0; t < nown; ++t) {
+          const int64_t r = own_row(t) + lane;
+          if (r >= i && r < k) s += u[t * 32 + lane] * col[r];
+        }
+        s = warp_sum(s);
+        if (lane == 0) p.wslot[(size_t)g * k + q] = s;
+      }
+    }
+    grid_sync(p.bar);
+    if (i + 1 < k) {
+      for (int64_t q = i + 1 + g + (int64_t)tid * G; q < k; q += (int64_t)G * 256) {
+        double s = 0.0;
+        for (int h = 0; h < G; ++h) s += p.wslot[(size_t)h * k + q];
+        p.w[q] = s * tau_u;
+      }
+    }
+    grid_sync(p.bar);
+    if (i + 1 >= k) break;
+    // ---- apply left reflector: M[r, q] -= u_r w_q ----
+    for (int64_t q = i + 1 + warp; q < k; q += 8) {
+      double* col = M + q * ld;
+      const double wq = p.w[q];
+      for (int64_t t = t0; t < nown; ++t) {
+        const int64_t r = own_row(t) + lane;
+        if (r >= i && r < k) col[r] -= u[t * 32 + lane] * wq;
+      }
+    }
+    __syncthreads();
+    // ---- right reflector from row i (owner CTA) ----
+    const bool owner = ((i / 32) % G) == g;
+    if (owner) {
+      if (warp == 0) {
+        double s = 0.0;
+        for (int64_t q = i + 2 + lane; q < k; q += 32) { const double x = M[i + q * ld]; s += x * x; }
+        s = warp_sum(s);
+        const double alpha = M[i + (i + 1) * ld];
+        double tau = 0.0, scal = 0.0, beta = alpha;
+        if (s > 0.0) {
+          beta = -copysign(sqrt(alpha * alpha + s), alpha);
+          tau = (beta - alpha) / beta;
+          scal = 1.0 / (alpha - beta);
+        }
+        for (int64_t q = i + 2 + lane; q < k; q += 32) p.v[q] = M[i + q * ld] * scal;
+        if (lane == 0) {
+          p.v[i + 1] = 1.0;
+          p.scal[0] = tau;
+          p.e[i] = beta;
+        }
+      }
+    }
+    grid_sync(p.bar);
+    const double tau_v = p.scal[0];
+    // ---- z = M v for own rows r > i, then M[r, q] -= z_r v_q ----
+    for (int64_t e = tid; e < 8 * nown * 32; e += 256) zp[e] = 0.0;
+    __syncthreads();
+    for (int64_t q = i + 1 + warp; q < k; q += 8) {
+      const double* col = M + q * ld;
+      const double vq = p.v[q];
+      for (int64_t t = t0; t < nown; ++t) {
+        const int64_t r = own_row(t) + lane;
+        if (r > i && r < k) zp[warp * nown * 32 + t * 32 + lane] += col[r] * vq;
+      }
+    }
+    __syncthreads();
+    for (int64_t e = tid; e < nown * 32; e += 256) {
+      double s = 0.0;
+      for (int w = 0; w < 8; ++w) s += zp[w * nown * 32 + e];
+      u[e] = s * tau_v;  // reuse u as z
+    }
+    __syncthreads();
+    double nrm = 0.0;
+    for (int64_t q = i + 1 + warp; q < k; q += 8) {
+      double* col = M + q * ld;
+      const double vq = p.v[q];
+      for (int64_t t = t0; t < nown; ++t) {
+        const int64_t r = own_row(t) + lane;
+        if (r > i && r < k) {
+          const double x = col[r] - u[t * 32 + lane] * vq;
+          col[r] = x;
+          if (q == i + 1 && r > i + 1) nrm += x * x;
+        }
+      }
+    }
+    // partial norm of column i+1 (rows > i+1): owned by the warp with q == i+1 (warp 0)
+    nrm = warp_sum(nrm);
+    if (tid == 0) p.nslot[g] = nrm;
+    grid_sync(p.bar);
+  }
+}
+
+// ---- bisection on the TGK matrix of the upper bidiagonal (d, e) ----------------------------
+// count_less(x) = #singular values < x (x > 0): Sturm count of TGK − xI over the off-diagonal
+// sequence d0, e0, d1, e1, ..., d_{k-1}; TGK has eigenvalues ±σ_i.
+__device__ int64_t count_less(const double* __restrict__ d, const double* __restrict__ e, int64_t k,
+                              double x, double pivmin) {
+  double q = -x;
+  int64_t neg = q < 0.0;
+  for (int64_t t = 1; t < 2 * k; ++t) {
+    const double a = (t & 1) ? d[(t - 1) >> 1] : e[(t - 2) >> 1];
+    if (fabs(q) < pivmin) q = -pivmin;
+    q = -x - (a * a) / q;
+    neg += q < 0.0;
+  }
+  return neg - k;
+}
+
+// j-th largest singular value (1-based) by 32-way multisection within [lo, hi] (warp-wide).
+__device__ double kth_largest(const double* d, const double* e, int64_t k, int64_t j, double lo,
+                              double hi, double pivmin) {
+  const int lane = threadIdx.x & 31;
+  const int64_t need = k - j + 1;  // σ_(j) = inf{x : count_less(x) >= need}
+  for (int it = 0; it < 40; ++it) {
+    if (!(hi - lo > 4e-16 * hi)) break;
+    const double x = lo + (hi - lo) * (double)(lane + 1) / 33.0;
+    const bool pred = count_less(d, e, k, x, pivmin) >= need;
+    const unsigned mask = __ballot_sync(0xffffffffu, pred);
+    const int first = mask ? __ffs(mask) - 1 : 32;
+    const double nlo = first == 0 ? lo : lo + (hi - lo) * (double)first / 33.0;
+    const double nhi = first == 32 ? hi : lo + (hi - lo) * (double)(first + 1) / 33.0;
+    lo = __shfl_sync(0xffffffffu, nlo, 0);
+    hi = __shfl_sync(0xffffffffu, nhi, 0);
+  }
+  return 0.5 * (lo + hi);
+}
+
+__device__ double tgk_bounds(const double* d, const double* e, int64_t k, double* pivmin) {
+  double ub = 0.0, amax2 = 0.0;
+  double prev = 0.0;
+  for (int64_t t = 1; t < 2 * k; ++t) {
+    const double a = fabs((t & 1) ? d[(t - 1) >> 1] : e[(t - 2) >> 1]);
+    ub = fmax(ub, prev + a);
+    prev = a;
+    amax2 = fmax(amax2, a * a);
+  }
+  ub = fmax(ub, prev);
+  *pivmin = 1e-290 * fmax(1.0, amax2);
+  return ub * (1.0 + 1e-14) + 1e-300;
+}
+
+__global__ void sigma_queries_kernel(const double* __restrict__ d, const double* __restrict__ e,
+                                     int64_t k, const SigmaQuery* __restrict__ q, int nq,
+                                     SigmaAnswer* __restrict__ out) {
+  __shared__ double sh_s1, sh_pivmin, sh_ub;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (warp == 0) {
+    double pivmin = 0.0, ub = 0.0;
+    if (lane == 0) ub = tgk_bounds(d, e, k, &pivmin);
+    ub = __shfl_sync(0xffffffffu, ub, 0);
+    pivmin = __shfl_sync(0xffffffffu, pivmin, 0);
+    const double s1 = k > 0 ? kth_largest(d, e, k, 1, 0.0, ub, pivmin) : 0.0;
+    if (lane == 0) { sh_s1 = s1; sh_pivmin = pivmin; sh_ub = ub; }
+  }
+  __syncthreads();
+  const double s1 = sh_s1, pivmin = sh_pivmin;
+  for (int qi = warp; qi < nq; qi += blockDim.x / 32) {
+    const double thr = q[qi].tol * s1;
+    const double xp = nextafter(thr, 1e308);
+    int64_t p = k - count_less(d, e, k, xp, pivmin);
+    const double thr2 = thr * thr - q[qi].delta * q[qi].delta;
+    const double thr_hi = thr2 > 0.0 ? sqrt(thr2) : 0.0;
+    const int64_t phi = thr_hi > 0.0 ? k - count_less(d, e, k, nextafter(thr_hi, 1e308), pivmin) : k;
+    double sp = 0.0, sp1 = 0.0;
+    if (p >= 1) sp = kth_largest(d, e, k, p, thr, sh_ub, pivmin);
+    if (p + 1 <= k) sp1 = kth_largest(d, e, k, p + 1, 0.0, xp, pivmin);
+    if (lane == 0) {
+      out[qi].sigma1 = s1;
+      out[qi].sigma_p = sp;
+      out[qi].sigma_p1 = sp1;
+      out[qi].rank_lo = (int)p;
+      out[qi].rank_hi = (int)phi;
+    }
+  }
+}
+
+// All singular values (descending), one warp per value — test/diagnostic path.
+__global__ void sigma_all_kernel(const double* __restrict__ d, const double* __restrict__ e,
+                                 int64_t k, double sigma_max, double* __restrict__ out) {
+  const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / 32;
+  if (wid >= k) return;
+  double pivmin = 1e-290;
+  const double ub = sigma_max * (1.0 + 1e-12) + 1e-300;
+  out[wid] = kth_largest(d, e, k, wid + 1, 0.0, ub, pivmin);
+}
+
+}  // namespace hb

@@ -1,0 +1,326 @@
+"""ctypes binding of the C ABI in include/hb.h (libhb200.so, sm_100a).
+
+This is the Python stub a maintainer would add on the reference side; tests and
+bench.py call the product only through it.  There is no CPU fallback: if the CUDA library is
+missing or no GPU is present, every entry point raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+from pathlib import Path
+from typing import Sequence
+
+PKG = Path(__file__).resolve().parent
+LIB_PATH = PKG / "lib" / "libhb200.so"
+
+# status codes (hb.h)
+OK, EINVAL, EDOMAIN, ECAP, ESINGULAR, EUNSUPPORTED, ENOMEM, ECUDA, ENCCL = range(9)
+STATUS_NAMES = ["OK", "EINVAL", "EDOMAIN", "ECAP", "ESINGULAR", "EUNSUPPORTED", "ENOMEM", "ECUDA",
+                "ENCCL"]
+
+# KernelId order of kernel.hpp:19-32; names of kernel_from_string (kernel.hpp:112-129)
+KERNEL_IDS = {
+    "one_over_r": 0, "log_r": 1, "helmholtz3d_re": 2, "helmholtz3d_im": 3,
+    "hankel_h12_re": 4, "hankel_h12_im": 5, "r": 6, "sin_r": 7,
+    "inv_sqrt_1_plus_r": 8, "exp_neg_r": 9, "exp_neg_r2": 10, "custom": 11,
+}
+KERNEL_NAMES = {v: k for k, v in KERNEL_IDS.items()}
+# KernelSpec::catalog diagonal values (kernel.hpp:46-61)
+CATALOG_DIAG = {0: 0.0, 1: 0.0, 2: 0.0, 5: 0.0, 3: 1.0, 8: 1.0, 9: 1.0, 10: 1.0, 4: 0.0, 6: 0.0,
+                7: 0.0}
+UNIFORM, GRID_INTERIOR, GRID_CLOSED = 0, 1, 2
+MAX_TOLS = 4
+
+
+class HBError(RuntimeError):
+    def __init__(self, status: int, where: str, detail: str = ""):
+        name = STATUS_NAMES[status] if 0 <= status < len(STATUS_NAMES) else str(status)
+        super().__init__(f"{where}: {name}" + (f" ({detail})" if detail else ""))
+        self.status = status
+
+
+class hb_kernel(ctypes.Structure):
+    _fields_ = [("id", ctypes.c_int32), ("has_diag", ctypes.c_int32), ("diag", ctypes.c_double)]
+
+
+class hb_cube(ctypes.Structure):
+    _fields_ = [("d", ctypes.c_int32), ("reserved", ctypes.c_int32),
+                ("lower", ctypes.c_double * 8), ("side", ctypes.c_double)]
+
+
+class hb_pair(ctypes.Structure):
+    _fields_ = [("target", hb_cube), ("source", hb_cube), ("d_prime", ctypes.c_int32),
+                ("point_mode", ctypes.c_int32), ("n_target", ctypes.c_int64),
+                ("n_source", ctypes.c_int64), ("seed", ctypes.c_uint64)]
+
+
+class hb_rank_result(ctypes.Structure):
+    _fields_ = [("rank", ctypes.c_int32), ("rank_lo", ctypes.c_int32), ("rank_hi", ctypes.c_int32),
+                ("k_factored", ctypes.c_int32), ("sigma1", ctypes.c_double),
+                ("sigma_r", ctypes.c_double), ("sigma_r1", ctypes.c_double),
+                ("gap", ctypes.c_double), ("resid", ctypes.c_double),
+                ("sec", ctypes.c_double * 4)]
+
+    def as_dict(self) -> dict:
+        return {f: (list(getattr(self, f)) if f == "sec" else getattr(self, f))
+                for f, _ in self._fields_}
+
+
+class hb_problem(ctypes.Structure):
+    _fields_ = [("kernel", hb_kernel), ("pair", hb_pair), ("tols", ctypes.c_double * MAX_TOLS),
+                ("ntol", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+
+
+# every symbol include/hb.h declares (checked by tests/test_abi.py)
+EXPORTS = [
+    "hb_version", "hb_status_string", "hb_last_error", "hb_context_create", "hb_context_destroy",
+    "hb_context_stream", "hb_context_set_tuning", "hb_generate_points", "hb_assemble",
+    "hb_eval_radial_host", "hb_rank_matrix", "hb_rank", "hb_last_sigma", "hb_sweep",
+    "hb_partition", "hb_problem_seed",
+]
+
+_lib = None
+
+
+def load(path: os.PathLike | str | None = None):
+    """Load libhb200.so (raises if it was not built — there is no fallback)."""
+    global _lib
+    if _lib is not None and path is None:
+        return _lib
+    p = Path(path) if path else LIB_PATH
+    if not p.exists():
+        raise FileNotFoundError(f"{p} is missing: run `make -C paper_2209_05819_b200` "
+                                f"(or __graft_entry__.build())")
+    L = ctypes.CDLL(str(p))
+    c_p = ctypes.c_void_p
+    L.hb_version.restype = ctypes.c_char_p
+    L.hb_status_string.restype = ctypes.c_char_p
+    L.hb_status_string.argtypes = [ctypes.c_int]
+    L.hb_last_error.restype = ctypes.c_char_p
+    L.hb_last_error.argtypes = [c_p]
+    L.hb_context_create.argtypes = [ctypes.c_int, ctypes.POINTER(c_p)]
+    L.hb_context_destroy.argtypes = [c_p]
+    L.hb_context_destroy.restype = None
+    L.hb_context_stream.argtypes = [c_p]
+    L.hb_context_stream.restype = c_p
+    L.hb_context_set_tuning.argtypes = [c_p, ctypes.c_int32, ctypes.c_double]
+    L.hb_generate_points.argtypes = [c_p, ctypes.POINTER(hb_pair), c_p, c_p]
+    L.hb_assemble.argtypes = [c_p, ctypes.POINTER(hb_kernel), c_p, ctypes.c_int64, c_p,
+                              ctypes.c_int64, ctypes.c_int32, c_p, ctypes.c_int64]
+    L.hb_eval_radial_host.argtypes = [ctypes.POINTER(hb_kernel), ctypes.c_double,
+                                      ctypes.POINTER(ctypes.c_double)]
+    L.hb_rank_matrix.argtypes = [c_p, c_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
+                                 ctypes.POINTER(ctypes.c_double), ctypes.c_int32,
+                                 ctypes.POINTER(hb_rank_result)]
+    L.hb_rank.argtypes = [c_p, ctypes.POINTER(hb_kernel), ctypes.POINTER(hb_pair),
+                          ctypes.POINTER(ctypes.c_double), ctypes.c_int32,
+                          ctypes.POINTER(hb_rank_result)]
+    L.hb_last_sigma.argtypes = [c_p, ctypes.POINTER(ctypes.c_double), ctypes.c_int64,
+                                ctypes.POINTER(ctypes.c_int64)]
+    L.hb_sweep.argtypes = [ctypes.POINTER(hb_problem), ctypes.c_int64,
+                           ctypes.POINTER(ctypes.c_int32), ctypes.c_int32,
+                           ctypes.POINTER(hb_rank_result), ctypes.POINTER(ctypes.c_int32)]
+    L.hb_partition.argtypes = [ctypes.POINTER(hb_problem), ctypes.c_int64, ctypes.c_int32,
+                               ctypes.POINTER(ctypes.c_int32)]
+    L.hb_problem_seed.argtypes = [ctypes.c_uint64, ctypes.c_int32, ctypes.c_int32, ctypes.c_int64]
+    L.hb_problem_seed.restype = ctypes.c_uint64
+    for name in ("hb_context_create", "hb_context_set_tuning", "hb_generate_points",
+                 "hb_assemble", "hb_eval_radial_host", "hb_rank_matrix", "hb_rank",
+                 "hb_last_sigma", "hb_sweep", "hb_partition"):
+        getattr(L, name).restype = ctypes.c_int
+    if path is None:
+        _lib = L
+    return L
+
+
+def _check(status: int, where: str, ctx=None):
+    if status != OK:
+        L = load()
+        detail = L.hb_last_error(ctx).decode() if ctx is not None else L.hb_last_error(None).decode()
+        raise HBError(status, where, detail)
+
+
+# ---- descriptors mirroring the reference value types ------------------------------------------
+
+def make_kernel(name_or_id, diagonal: float | None = "catalog") -> hb_kernel:
+    """KernelSpec::catalog(id) (kernel.hpp:40-67); diagonal=None -> no diagonal value."""
+    kid = KERNEL_IDS[name_or_id] if isinstance(name_or_id, str) else int(name_or_id)
+    k = hb_kernel()
+    k.id = kid
+    if diagonal == "catalog":
+        if kid in CATALOG_DIAG:
+            k.has_diag, k.diag = 1, CATALOG_DIAG[kid]
+    elif diagonal is not None:
+        k.has_diag, k.diag = 1, float(diagonal)
+    return k
+
+
+def make_cube(lower: Sequence[float], side: float = 1.0) -> hb_cube:
+    c = hb_cube()
+    c.d = len(lower)
+    for i, v in enumerate(lower):
+        c.lower[i] = float(v)
+    c.side = float(side)
+    return c
+
+
+def offset(d: int, dprime: int | None) -> list[float]:
+    """Source-cube offset: far-field (2,0,..,0); d'-surface: d-d' leading ones."""
+    o = [0.0] * d
+    if dprime is None or dprime < 0:
+        o[0] = 2.0
+    else:
+        for i in range(d - dprime):
+            o[i] = 1.0
+    return o
+
+
+def make_pair(d: int, dprime: int | None, n: int, mode: int = UNIFORM, seed: int = 0,
+              n_source: int | None = None) -> hb_pair:
+    p = hb_pair()
+    p.target = make_cube([0.0] * d)
+    p.source = make_cube(offset(d, dprime))
+    p.d_prime = -1 if dprime is None else int(dprime)
+    p.point_mode = mode
+    p.n_target = n
+    p.n_source = n if n_source is None else n_source
+    p.seed = seed & 0xFFFFFFFFFFFFFFFF
+    return p
+
+
+def problem_seed(base: int, d: int, dprime: int | None, n: int) -> int:
+    return int(load().hb_problem_seed(base & 0xFFFFFFFFFFFFFFFF, d,
+                                      -1 if dprime is None else dprime, n))
+
+
+def make_problem(kernel: str, d: int, dprime: int | None, n: int, tols: Sequence[float],
+                 mode: int = UNIFORM, seed: int | None = None, base_seed: int = 0) -> hb_problem:
+    pr = hb_problem()
+    pr.kernel = make_kernel(kernel)
+    s = problem_seed(base_seed, d, dprime, n) if seed is None else seed
+    pr.pair = make_pair(d, dprime, n, mode, s)
+    for i, t in enumerate(tols):
+        pr.tols[i] = float(t)
+    pr.ntol = len(tols)
+    return pr
+
+
+def eval_radial_host(kernel: hb_kernel, r: float) -> float:
+    out = ctypes.c_double()
+    _check(load().hb_eval_radial_host(ctypes.byref(kernel), float(r), ctypes.byref(out)),
+           "hb_eval_radial_host")
+    return out.value
+
+
+@dataclass
+class RankResult:
+    rank: int
+    rank_lo: int
+    rank_hi: int
+    k_factored: int
+    sigma1: float
+    sigma_r: float
+    sigma_r1: float
+    gap: float
+    resid: float
+    sec: list
+
+    @classmethod
+    def of(cls, r: hb_rank_result) -> "RankResult":
+        return cls(r.rank, r.rank_lo, r.rank_hi, r.k_factored, r.sigma1, r.sigma_r, r.sigma_r1,
+                   r.gap, r.resid, list(r.sec))
+
+
+class Context:
+    """One device, one CUDA stream (hb_context)."""
+
+    def __init__(self, device: int = 0):
+        self._lib = load()
+        self._h = ctypes.c_void_p()
+        _check(self._lib.hb_context_create(device, ctypes.byref(self._h)), "hb_context_create")
+        self.device = device
+
+    def close(self):
+        if self._h:
+            self._lib.hb_context_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def stream(self) -> int:
+        return int(self._lib.hb_context_stream(self._h) or 0)
+
+    def set_tuning(self, block_max: int = 120, eta: float = 0.01):
+        _check(self._lib.hb_context_set_tuning(self._h, block_max, eta), "set_tuning", self._h)
+
+    def generate_points(self, pair: hb_pair, d_tgt_ptr: int, d_src_ptr: int):
+        _check(self._lib.hb_generate_points(self._h, ctypes.byref(pair), d_tgt_ptr, d_src_ptr),
+               "hb_generate_points", self._h)
+
+    def assemble(self, kernel: hb_kernel, d_tgt: int, T: int, d_src: int, N: int, d: int,
+                 d_K: int, ldk: int):
+        _check(self._lib.hb_assemble(self._h, ctypes.byref(kernel), d_tgt, T, d_src, N, d, d_K,
+                                     ldk), "hb_assemble", self._h)
+
+    def rank(self, kernel: hb_kernel, pair: hb_pair, tols: Sequence[float]) -> list[RankResult]:
+        nt = len(tols)
+        ct = (ctypes.c_double * nt)(*tols)
+        out = (hb_rank_result * nt)()
+        _check(self._lib.hb_rank(self._h, ctypes.byref(kernel), ctypes.byref(pair), ct, nt, out),
+               "hb_rank", self._h)
+        return [RankResult.of(o) for o in out]
+
+    def rank_matrix(self, d_A: int, m: int, n: int, ld: int, tols: Sequence[float]):
+        nt = len(tols)
+        ct = (ctypes.c_double * nt)(*tols)
+        out = (hb_rank_result * nt)()
+        _check(self._lib.hb_rank_matrix(self._h, d_A, m, n, ld, ct, nt, out), "hb_rank_matrix",
+               self._h)
+        return [RankResult.of(o) for o in out]
+
+    def last_sigma(self, max_count: int | None = None) -> list[float]:
+        cnt = ctypes.c_int64()
+        _check(self._lib.hb_last_sigma(self._h, None, 0, ctypes.byref(cnt)), "hb_last_sigma",
+               self._h)
+        k = cnt.value if max_count is None else min(cnt.value, max_count)
+        buf = (ctypes.c_double * max(k, 1))()
+        _check(self._lib.hb_last_sigma(self._h, buf, k, ctypes.byref(cnt)), "hb_last_sigma",
+               self._h)
+        return list(buf[:k])
+
+
+def partition(problems: Sequence[hb_problem], nparts: int) -> list[int]:
+    n = len(problems)
+    arr = (hb_problem * max(n, 1))(*problems)
+    own = (ctypes.c_int32 * max(n, 1))()
+    _check(load().hb_partition(arr, n, nparts, own), "hb_partition")
+    return list(own[:n])
+
+
+def sweep(problems: Sequence[hb_problem], devices: Sequence[int] = (0,)):
+    """hb_sweep: returns (results per problem [list per tol], statuses)."""
+    n = len(problems)
+    arr = (hb_problem * max(n, 1))(*problems)
+    total = sum(p.ntol for p in problems)
+    out = (hb_rank_result * max(total, 1))()
+    st = (ctypes.c_int32 * max(n, 1))()
+    devs = (ctypes.c_int32 * len(devices))(*devices)
+    load().hb_sweep(arr, n, devs, len(devices), out, st)
+    res, o = [], 0
+    for p in problems:
+        res.append([RankResult.of(out[o + t]) for t in range(p.ntol)])
+        o += p.ntol
+    return res, list(st[:n])
