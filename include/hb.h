@@ -158,6 +158,41 @@ hb_status hb_last_sigma(hb_context* ctx, double* host_out, int64_t max, int64_t*
 hb_status hb_sweep(const hb_problem* probs, int64_t n, const int32_t* devices, int32_t ndev,
                    hb_rank_result* out, int32_t* status_out);
 
+/* ---- profiling: per-phase device time from CUDA events on the context stream (off by
+ * default; the events add ~µs per phase) and the process-wide kernel-launch counter ---------- */
+enum {
+  HB_PH_ASSEMBLY = 0, HB_PH_SKETCH = 1, HB_PH_PIVOT = 2, HB_PH_PANEL = 3, HB_PH_UPDATE = 4,
+  HB_PH_DOWNDATE = 5, HB_PH_SIGMA1 = 6, HB_PH_CERT_QR = 7, HB_PH_BIDIAG = 8, HB_PH_BISECT = 9,
+  HB_NPHASE = 10
+};
+typedef struct {
+  double phase_ms[HB_NPHASE];
+  double gemm_ms;         /* device time inside the FP64 DMMA GEMM launches (incl. split-K finish) */
+  double gemm_flops;      /* sum of 2*M*N*K over those launches */
+  uint64_t gemm_launches;
+  uint64_t launches;      /* every kernel launch issued by the library (process-wide counter) */
+  uint64_t problems;      /* problems completed with profiling on */
+} hb_stats;
+const char* hb_phase_name(int32_t phase);
+hb_status hb_context_set_profiling(hb_context* ctx, int32_t on);
+/* ctx == NULL: process-wide totals (all contexts, including hb_sweep workers). */
+hb_status hb_stats_get(const hb_context* ctx, hb_stats* out);
+hb_status hb_stats_reset(hb_context* ctx);
+
+/* hb_sweep with options.  Workers reuse one cached context per device across calls (workspace
+ * stays allocated); device_seconds[w] = device time of worker w's problem list, measured with
+ * CUDA events on its stream (first launch to last completion). */
+#define HB_MAX_DEVICES 64
+typedef struct {
+  int32_t profiling;
+  int32_t reserved;
+  double device_seconds[HB_MAX_DEVICES];
+} hb_sweep_opts;
+hb_status hb_sweep_ex(const hb_problem* probs, int64_t n, const int32_t* devices, int32_t ndev,
+                      hb_rank_result* out, int32_t* status_out, hb_sweep_opts* opts);
+/* Free the per-device contexts cached by hb_sweep / hb_sweep_ex. */
+void hb_sweep_release(void);
+
 /* LPT assignment used by hb_sweep / multi-process sweeps: owner[i] in [0, nparts). */
 hb_status hb_partition(const hb_problem* probs, int64_t n, int32_t nparts, int32_t* owner);
 

@@ -9,5 +9,5 @@ from .hb import (  # noqa: F401
     CATALOG_DIAG, EXPORTS, GRID_CLOSED, GRID_INTERIOR, KERNEL_IDS, KERNEL_NAMES, LIB_PATH,
     UNIFORM, Context, HBError, RankResult, eval_radial_host, hb_kernel, hb_pair, hb_problem,
     hb_rank_result, load, make_cube, make_kernel, make_pair, make_problem, offset, partition,
-    problem_seed, sweep,
+    problem_seed, sweep, global_stats, reset_global_stats, sweep_release, hb_stats, PHASES,
 )

@@ -134,6 +134,7 @@ void rank_pair(hb_context* c, const hb_kernel* kernel, const hb_pair* pair, cons
   if ((double)lda * n * 8.0 * 1.25 > (double)total_b)
     throw Error(HB_ENOMEM, "K does not fit in device memory");
   HB_CUDA(cudaEventRecord(c->ev[0], c->stream));
+  hb::Phase ph(c, HB_PH_ASSEMBLY);
   double* X = hb::ws<double>(c, hb::B_X, (size_t)d * m);
   double* Yp = hb::ws<double>(c, hb::B_Y, (size_t)d * n);
   double* A = hb::ws<double>(c, hb::B_A, (size_t)lda * n);
@@ -142,6 +143,7 @@ void rank_pair(hb_context* c, const hb_kernel* kernel, const hb_pair* pair, cons
   gen_points(c, pair, X, Yp);
   hb::launch_assemble(*kernel, X, m, Yp, n, d, A, lda, flags, c->stream);
   HB_CUDA(cudaEventRecord(c->ev[4], c->stream));
+  ph.close();
   raise_flags(read_flags(c, flags));
   float fm = 0, cm = 0;
   hb::rank_matrix_inplace(c, A, m, n, lda, tols, ntol, out, &fm, &cm);
@@ -173,6 +175,20 @@ double problem_cost(const hb_problem& p) {
   const double n = (double)std::max(p.pair.n_target, p.pair.n_source);
   const double pr = std::min(n, 1.4 * predicted_rank(p.pair.target.d, p.pair.d_prime, (int64_t)n) + 32.0);
   return n * n * (60.0 + 4.0 * pr) + 30.0 * pr * pr * pr;
+}
+
+// live contexts (for process-wide stats) and the per-device cache used by hb_sweep
+std::mutex g_reg_mu;
+std::vector<hb_context*> g_live;
+hb_stats g_retired{};
+std::vector<std::pair<std::pair<int, int>, hb_context*>> g_cache;  // ((device, slot), ctx)
+
+void add_stats(hb_stats& a, const hb_stats& b) {
+  for (int i = 0; i < HB_NPHASE; ++i) a.phase_ms[i] += b.phase_ms[i];
+  a.gemm_ms += b.gemm_ms;
+  a.gemm_flops += b.gemm_flops;
+  a.gemm_launches += b.gemm_launches;
+  a.problems += b.problems;
 }
 
 }  // namespace
@@ -220,14 +236,61 @@ hb_status hb_context_create(int device, hb_context** out) {
     delete c;
     return s;
   }
+  {
+    std::lock_guard<std::mutex> lk(g_reg_mu);
+    g_live.push_back(c);
+  }
   *out = c;
   return HB_OK;
 }
 
 void hb_context_destroy(hb_context* ctx) {
   if (!ctx) return;
+  {
+    std::lock_guard<std::mutex> lk(g_reg_mu);
+    add_stats(g_retired, ctx->stats);
+    g_live.erase(std::remove(g_live.begin(), g_live.end(), ctx), g_live.end());
+  }
   hb::context_free(ctx);
   delete ctx;
+}
+
+const char* hb_phase_name(int32_t ph) {
+  static const char* names[HB_NPHASE] = {"assembly", "sketch", "pivot", "panel", "update",
+                                         "downdate", "sigma1", "cert_qr", "bidiag", "bisect"};
+  return (ph >= 0 && ph < HB_NPHASE) ? names[ph] : "?";
+}
+
+hb_status hb_context_set_profiling(hb_context* ctx, int32_t on) {
+  if (!ctx) return HB_EINVAL;
+  ctx->profiling = on != 0;
+  return HB_OK;
+}
+
+hb_status hb_stats_get(const hb_context* ctx, hb_stats* out) {
+  if (!out) return HB_EINVAL;
+  hb_stats s{};
+  if (ctx) {
+    s = ctx->stats;
+  } else {
+    std::lock_guard<std::mutex> lk(g_reg_mu);
+    s = g_retired;
+    for (auto* c : g_live) add_stats(s, c->stats);
+  }
+  s.launches = hb::launch_counter().load();
+  *out = s;
+  return HB_OK;
+}
+
+hb_status hb_stats_reset(hb_context* ctx) {
+  if (ctx) {
+    ctx->stats = hb_stats{};
+  } else {
+    std::lock_guard<std::mutex> lk(g_reg_mu);
+    g_retired = hb_stats{};
+    for (auto* c : g_live) c->stats = hb_stats{};
+  }
+  return HB_OK;
 }
 
 void* hb_context_stream(hb_context* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
@@ -362,9 +425,34 @@ hb_status hb_partition(const hb_problem* probs, int64_t n, int32_t nparts, int32
   return HB_OK;
 }
 
-hb_status hb_sweep(const hb_problem* probs, int64_t n, const int32_t* devices, int32_t ndev,
-                   hb_rank_result* out, int32_t* status_out) {
-  if (n < 0 || (n > 0 && (!probs || !out)) || ndev < 1 || !devices) return HB_EINVAL;
+static hb_context* cached_context(int device, int slot, hb_status* st) {
+  {
+    std::lock_guard<std::mutex> lk(g_reg_mu);
+    for (auto& e : g_cache)
+      if (e.first.first == device && e.first.second == slot) return e.second;
+  }
+  hb_context* c = nullptr;
+  *st = hb_context_create(device, &c);
+  if (*st != HB_OK) return nullptr;
+  std::lock_guard<std::mutex> lk(g_reg_mu);
+  g_cache.push_back({{device, slot}, c});
+  return c;
+}
+
+void hb_sweep_release(void) {
+  std::vector<hb_context*> cs;
+  {
+    std::lock_guard<std::mutex> lk(g_reg_mu);
+    for (auto& e : g_cache) cs.push_back(e.second);
+    g_cache.clear();
+  }
+  for (auto* c : cs) hb_context_destroy(c);
+}
+
+hb_status hb_sweep_ex(const hb_problem* probs, int64_t n, const int32_t* devices, int32_t ndev,
+                      hb_rank_result* out, int32_t* status_out, hb_sweep_opts* opts) {
+  if (n < 0 || (n > 0 && (!probs || !out)) || ndev < 1 || ndev > HB_MAX_DEVICES || !devices)
+    return HB_EINVAL;
   std::vector<int64_t> offset(n + 1, 0);
   for (int64_t i = 0; i < n; ++i) {
     if (probs[i].ntol < 1 || probs[i].ntol > HB_MAX_TOLS) return HB_EINVAL;
@@ -375,25 +463,38 @@ hb_status hb_sweep(const hb_problem* probs, int64_t n, const int32_t* devices, i
   std::vector<hb_status> st(n, HB_OK);
   std::vector<double> cost(n);
   for (int64_t i = 0; i < n; ++i) cost[i] = problem_cost(probs[i]);
-  std::vector<hb_status> dev_status(ndev, HB_OK);
+  std::vector<int> slot(ndev, 0);
+  for (int w = 0; w < ndev; ++w)
+    for (int v = 0; v < w; ++v)
+      if (devices[v] == devices[w]) slot[w]++;
   auto worker = [&](int w) {
-    hb_context* c = nullptr;
-    hb_status s = hb_context_create(devices[w], &c);
-    if (s != HB_OK) {
-      dev_status[w] = s;
+    hb_status cs = HB_OK;
+    hb_context* c = cached_context(devices[w], slot[w], &cs);
+    if (!c) {
       for (int64_t i = 0; i < n; ++i)
-        if (owner[i] == w) st[i] = s;
+        if (owner[i] == w) st[i] = cs;
       return;
     }
+    if (opts) c->profiling = opts->profiling != 0;
     std::vector<int64_t> mine;
     for (int64_t i = 0; i < n; ++i)
       if (owner[i] == w) mine.push_back(i);
     std::stable_sort(mine.begin(), mine.end(), [&](int64_t a, int64_t b) { return cost[a] > cost[b]; });
+    cudaSetDevice(c->device);
+    cudaEventRecord(c->ev[5], c->stream);
     for (int64_t i : mine) {
       const hb_problem& p = probs[i];
       st[i] = hb_rank(c, &p.kernel, &p.pair, p.tols, p.ntol, out + offset[i]);
     }
-    hb_context_destroy(c);
+    // device span of this worker: first event to last completion on its stream
+    cudaEvent_t end;
+    cudaEventCreate(&end);
+    cudaEventRecord(end, c->stream);
+    cudaEventSynchronize(end);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, c->ev[5], end);
+    cudaEventDestroy(end);
+    if (opts) opts->device_seconds[w] = ms * 1e-3;
   };
   std::vector<std::thread> th;
   for (int w = 1; w < ndev; ++w) th.emplace_back(worker, w);
@@ -405,6 +506,11 @@ hb_status hb_sweep(const hb_problem* probs, int64_t n, const int32_t* devices, i
     if (first == HB_OK && st[i] != HB_OK) first = st[i];
   }
   return first;
+}
+
+hb_status hb_sweep(const hb_problem* probs, int64_t n, const int32_t* devices, int32_t ndev,
+                   hb_rank_result* out, int32_t* status_out) {
+  return hb_sweep_ex(probs, n, devices, ndev, out, status_out, nullptr);
 }
 
 }  // extern "C"

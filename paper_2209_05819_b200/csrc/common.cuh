@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
 #include <stdexcept>
 #include <string>
 
@@ -26,7 +27,17 @@ struct Error : std::runtime_error {
                             std::to_string(__LINE__));                                       \
   } while (0)
 
-#define HB_LAUNCH_CHECK() HB_CUDA(cudaGetLastError())
+// every kernel launch site of the library passes through here: the counter backs the
+// "gpu_launches" figure of bench.py (hb_stats.launches)
+inline std::atomic<unsigned long long>& launch_counter() {
+  static std::atomic<unsigned long long> n{0};
+  return n;
+}
+#define HB_LAUNCH_CHECK()                                         \
+  do {                                                            \
+    ::hb::launch_counter().fetch_add(1, std::memory_order_relaxed); \
+    HB_CUDA(cudaGetLastError());                                  \
+  } while (0)
 
 #define HB_REQUIRE(cond, st, msg) \
   do {                            \

@@ -25,6 +25,14 @@ struct hb_context {
   std::vector<Buf> bufs;
   cudaEvent_t ev[6] = {};
 
+  // profiling (hb_context_set_profiling)
+  bool profiling = false;
+  std::vector<cudaEvent_t> evpool;
+  size_t evused = 0;
+  struct Mark { int phase; size_t e0, e1; double flops; };
+  std::vector<Mark> marks;
+  hb_stats stats{};
+
   // last certification (for hb_last_sigma)
   int64_t last_k = 0;
   double last_sigma1 = 0.0;
@@ -51,6 +59,30 @@ T* ws(hb_context* c, int id, size_t elems) {
   }
   return static_cast<T*>(b.p);
 }
+
+// ---- profiling helpers (rank.cu) ----
+size_t prof_event(hb_context* c);                 // record a pooled event on the stream
+void prof_resolve(hb_context* c);                 // after a stream sync: fold marks into stats
+constexpr int PH_GEMM = -1;                       // mark kind for single GEMM launches
+struct Phase {
+  hb_context* c;
+  int ph;
+  size_t e0 = 0;
+  bool open = true;
+  Phase(hb_context* c_, int ph_) : c(c_), ph(ph_) {
+    if (c->profiling) e0 = prof_event(c);
+  }
+  void close() {
+    if (open && c->profiling) {
+      try {
+        c->marks.push_back({ph, e0, prof_event(c), 0.0});
+      } catch (...) {
+      }
+    }
+    open = false;
+  }
+  ~Phase() { close(); }
+};
 
 // Internal entry points (rank.cu).
 void rank_matrix_inplace(hb_context* c, double* A, int64_t m, int64_t n, int64_t lda,

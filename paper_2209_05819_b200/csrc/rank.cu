@@ -42,7 +42,11 @@ struct Gemm {
   hb_context* c;
   void operator()(const GemmArgs& g) {
     double* sk = ws<double>(c, B_SPLITK, kSplitKElems);
+    size_t e0 = 0;
+    if (c->profiling) e0 = prof_event(c);
     launch_dgemm(g, sk, kSplitKElems, c->num_sms, c->stream);
+    if (c->profiling)
+      c->marks.push_back({PH_GEMM, e0, prof_event(c), 2.0 * (double)g.M * (double)g.N * (double)g.K});
   }
   static constexpr int64_t kSplitKElems = 8ll << 20;
 };
@@ -152,7 +156,10 @@ void rank_matrix_inplace(hb_context* c, double* A, int64_t m, int64_t n, int64_t
   HB_LAUNCH_CHECK();
 
   uint64_t sketch_seed = 0x243F6A8885A308D3ull;
-  if (kmax > 0) sketch(c, A, lda, m, n, Y, sketch_seed);
+  if (kmax > 0) {
+    Phase ph(c, HB_PH_SKETCH);
+    sketch(c, A, lda, m, n, Y, sketch_seed);
+  }
 
   int64_t j = 0;
   int b = std::min(32, c->block_max);
@@ -169,12 +176,16 @@ void rank_matrix_inplace(hb_context* c, double* A, int64_t m, int64_t n, int64_t
     sp.stop_fro2 = sigma1_est > 0.0 ? stop_res * stop_res : -1.0;
     sp.slots = sk_slots; sp.piv = piv; sp.swaps = swaps; sp.rdiag = rdiag; sp.out_est = est;
     sp.out_b = beff; sp.bar = barrier(c);
-    coop(sketch_cpqr_kernel, clampi(ceil_div(n_tr, 128), 1, c->num_sms), 0, st, sp);
+    {
+      Phase ph(c, HB_PH_PIVOT);
+      coop(sketch_cpqr_kernel, clampi(ceil_div(n_tr, 128), 1, c->num_sms), 0, st, sp);
+    }
     int bh = 0;
     sync_to_host(c, beff, &bh, sizeof(int));
     if (bh == 0) {
       // the sketch of the trailing matrix vanished: re-sketch once, else the trailing block is 0
       if (zero_retries++ < 1) {
+        Phase ph(c, HB_PH_SKETCH);
         sketch_seed = splitmix64(sketch_seed);
         double* Om = ws<double>(c, B_OMEGA, (size_t)ell * std::max<int64_t>(mp, 1));
         launch_gaussian(Om, ell, mp, ell, sketch_seed, st);
@@ -187,19 +198,28 @@ void rank_matrix_inplace(hb_context* c, double* A, int64_t m, int64_t n, int64_t
       break;
     }
     zero_retries = 0;
-    permute_kernel<<<(unsigned)ceil_div(m + ell + 1, 256), 256, 0, st>>>(A, lda, m, Y, ell, ell,
-                                                                           perm, j, swaps, beff);
-    HB_LAUNCH_CHECK();
+    {
+      Phase ph(c, HB_PH_PIVOT);
+      permute_kernel<<<(unsigned)ceil_div(m + ell + 1, 256), 256, 0, st>>>(A, lda, m, Y, ell, ell,
+                                                                             perm, j, swaps, beff);
+      HB_LAUNCH_CHECK();
+    }
     double* P = A + j + j * lda;
-    panel_and_T(c, P, lda, mp, bh, V, ldv, tau, T);
+    {
+      Phase ph(c, HB_PH_PANEL);
+      panel_and_T(c, P, lda, mp, bh, V, ldv, tau, T);
+    }
     const int64_t n2 = n - j - bh;
+    Phase ph_up(c, HB_PH_UPDATE);
     if (n2 > 0 && mp > bh) {
       apply_block_reflector(c, V, ldv, T, bh, A + j + (j + bh) * lda, lda, mp, n2, scal);
     } else {
       if (n2 > 0) apply_block_reflector(c, V, ldv, T, bh, A + j + (j + bh) * lda, lda, mp, n2, nullptr);
       HB_CUDA(cudaMemsetAsync(scal, 0, sizeof(double), st));
     }
+    ph_up.close();
     if (first) {
+      Phase ph(c, HB_PH_SIGMA1);
       PowerParams pw{};
       pw.R = A; pw.ld = lda; pw.b = bh; pw.n = n; pw.iters = 40;
       pw.slots = ws<double>(c, B_SIG1, (size_t)2 * c->num_sms * (kBlockMax + 1));
@@ -207,6 +227,7 @@ void rank_matrix_inplace(hb_context* c, double* A, int64_t m, int64_t n, int64_t
       coop(power_sigma1_kernel, clampi(ceil_div(n, 256), 1, c->num_sms), 0, st, pw);
     }
     if (n2 > 0) {
+      Phase ph(c, HB_PH_DOWNDATE);
       const size_t rsm = (size_t)bh * bh * sizeof(double);
       if (rsm > 48 * 1024)
         HB_CUDA(cudaFuncSetAttribute((const void*)sketch_trsm_kernel,
@@ -230,6 +251,7 @@ void rank_matrix_inplace(hb_context* c, double* A, int64_t m, int64_t n, int64_t
     if (delta <= c->eta * tol_min * sigma1_est) break;
     if (!(fro_at_sketch < INFINITY)) fro_at_sketch = delta;
     if (delta < 1e-8 * fro_at_sketch) {
+      Phase ph(c, HB_PH_SKETCH);
       // the downdated sketch has lost ~8 digits to cancellation: draw a fresh one
       sketch_seed = splitmix64(sketch_seed);
       const int64_t mr = m - j;
@@ -256,6 +278,7 @@ void rank_matrix_inplace(hb_context* c, double* A, int64_t m, int64_t n, int64_t
     const int64_t ldb = round_up(n, 8);
     double* Bc = ws<double>(c, B_CERT_B, (size_t)ldb * k);
     dim3 tb(32, 8), tg((unsigned)ceil_div(n, 32), (unsigned)ceil_div(k, 32));
+    Phase ph_qr(c, HB_PH_CERT_QR);
     transpose_upper_kernel<<<tg, tb, 0, st>>>(A, lda, k, n, Bc, ldb);
     HB_LAUNCH_CHECK();
     const int bq_max = kBlockMax;
@@ -271,6 +294,8 @@ void rank_matrix_inplace(hb_context* c, double* A, int64_t m, int64_t n, int64_t
     double* Mk = ws<double>(c, B_CERT_M, (size_t)ldm * k);
     copy_upper_kernel<<<(unsigned)ceil_div(k * k, 256), 256, 0, st>>>(Bc, ldb, k, Mk, ldm);
     HB_LAUNCH_CHECK();
+    ph_qr.close();
+    Phase ph_bd(c, HB_PH_BIDIAG);
     double* d = ws<double>(c, B_D, (size_t)k + 1);
     double* e = ws<double>(c, B_E, (size_t)k + 1);
     HB_CUDA(cudaMemsetAsync(e, 0, sizeof(double) * (k + 1), st));
@@ -288,6 +313,8 @@ void rank_matrix_inplace(hb_context* c, double* A, int64_t m, int64_t n, int64_t
     const size_t smem = (size_t)nown * 32 * 9 * sizeof(double);
     HB_REQUIRE(smem <= 200 * 1024, HB_ECAP, "bidiag: k too large");
     coop(bidiag_kernel, G, smem, st, bp);
+    ph_bd.close();
+    Phase ph_bs(c, HB_PH_BISECT);
     SigmaQuery* dq = ws<SigmaQuery>(c, B_QUERY, HB_MAX_TOLS);
     SigmaAnswer* da = ws<SigmaAnswer>(c, B_ANSWER, HB_MAX_TOLS);
     HB_CUDA(cudaMemcpyAsync(dq, hq, sizeof(SigmaQuery) * ntol, cudaMemcpyHostToDevice, st));
@@ -300,6 +327,10 @@ void rank_matrix_inplace(hb_context* c, double* A, int64_t m, int64_t n, int64_t
   float f_ms = 0.f, c_ms = 0.f;
   HB_CUDA(cudaEventElapsedTime(&f_ms, c->ev[1], c->ev[2]));
   HB_CUDA(cudaEventElapsedTime(&c_ms, c->ev[2], c->ev[3]));
+  if (c->profiling) {
+    prof_resolve(c);
+    c->stats.problems += 1;
+  }
   if (fact_ms) *fact_ms = f_ms;
   if (cert_ms) *cert_ms = c_ms;
   c->last_k = k;
@@ -325,6 +356,34 @@ void rank_matrix_inplace(hb_context* c, double* A, int64_t m, int64_t n, int64_t
     r.sec[1] = f_ms * 1e-3;
     r.sec[2] = c_ms * 1e-3;
   }
+}
+
+size_t prof_event(hb_context* c) {
+  if (c->evused == c->evpool.size()) {
+    cudaEvent_t e;
+    HB_CUDA(cudaEventCreate(&e));
+    c->evpool.push_back(e);
+  }
+  const size_t i = c->evused++;
+  HB_CUDA(cudaEventRecord(c->evpool[i], c->stream));
+  return i;
+}
+
+void prof_resolve(hb_context* c) {
+  if (!c->profiling && c->marks.empty()) return;
+  for (const auto& mk : c->marks) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, c->evpool[mk.e0], c->evpool[mk.e1]) != cudaSuccess) continue;
+    if (mk.phase == PH_GEMM) {
+      c->stats.gemm_ms += ms;
+      c->stats.gemm_flops += mk.flops;
+      c->stats.gemm_launches += 1;
+    } else if (mk.phase >= 0 && mk.phase < HB_NPHASE) {
+      c->stats.phase_ms[mk.phase] += ms;
+    }
+  }
+  c->marks.clear();
+  c->evused = 0;
 }
 
 void context_init(hb_context* c, int device) {
@@ -353,6 +412,7 @@ void context_free(hb_context* c) {
   if (c->pinned) cudaFreeHost(c->pinned);
   for (auto& e : c->ev)
     if (e) cudaEventDestroy(e);
+  for (auto& e : c->evpool) cudaEventDestroy(e);
   if (c->stream) cudaStreamDestroy(c->stream);
 }
 

@@ -68,6 +68,28 @@ class hb_rank_result(ctypes.Structure):
                 for f, _ in self._fields_}
 
 
+NPHASE = 10
+PHASES = ["assembly", "sketch", "pivot", "panel", "update", "downdate", "sigma1", "cert_qr",
+          "bidiag", "bisect"]
+MAX_DEVICES = 64
+
+
+class hb_stats(ctypes.Structure):
+    _fields_ = [("phase_ms", ctypes.c_double * NPHASE), ("gemm_ms", ctypes.c_double),
+                ("gemm_flops", ctypes.c_double), ("gemm_launches", ctypes.c_uint64),
+                ("launches", ctypes.c_uint64), ("problems", ctypes.c_uint64)]
+
+    def as_dict(self) -> dict:
+        return {"phase_ms": dict(zip(PHASES, list(self.phase_ms))), "gemm_ms": self.gemm_ms,
+                "gemm_flops": self.gemm_flops, "gemm_launches": self.gemm_launches,
+                "launches": self.launches, "problems": self.problems}
+
+
+class hb_sweep_opts(ctypes.Structure):
+    _fields_ = [("profiling", ctypes.c_int32), ("reserved", ctypes.c_int32),
+                ("device_seconds", ctypes.c_double * MAX_DEVICES)]
+
+
 class hb_problem(ctypes.Structure):
     _fields_ = [("kernel", hb_kernel), ("pair", hb_pair), ("tols", ctypes.c_double * MAX_TOLS),
                 ("ntol", ctypes.c_int32), ("reserved", ctypes.c_int32)]
@@ -78,7 +100,10 @@ EXPORTS = [
     "hb_version", "hb_status_string", "hb_last_error", "hb_context_create", "hb_context_destroy",
     "hb_context_stream", "hb_context_set_tuning", "hb_generate_points", "hb_assemble",
     "hb_eval_radial_host", "hb_rank_matrix", "hb_rank", "hb_last_sigma", "hb_sweep",
-    "hb_partition", "hb_problem_seed",
+    "hb_partition", "hb_problem_seed", "hb_phase_name", "hb_context_set_profiling",
+    "hb_stats_get", "hb_stats_reset", "hb_sweep_ex", "hb_sweep_release",
+    # include/hb_debug.h (test hooks)
+    "hb_debug_dgemm", "hb_debug_dgemm_async",
 ]
 
 _lib = None
@@ -126,9 +151,26 @@ def load(path: os.PathLike | str | None = None):
                                ctypes.POINTER(ctypes.c_int32)]
     L.hb_problem_seed.argtypes = [ctypes.c_uint64, ctypes.c_int32, ctypes.c_int32, ctypes.c_int64]
     L.hb_problem_seed.restype = ctypes.c_uint64
+    L.hb_phase_name.argtypes = [ctypes.c_int32]
+    L.hb_phase_name.restype = ctypes.c_char_p
+    L.hb_context_set_profiling.argtypes = [c_p, ctypes.c_int32]
+    L.hb_stats_get.argtypes = [c_p, ctypes.POINTER(hb_stats)]
+    L.hb_stats_reset.argtypes = [c_p]
+    L.hb_sweep_ex.argtypes = [ctypes.POINTER(hb_problem), ctypes.c_int64,
+                              ctypes.POINTER(ctypes.c_int32), ctypes.c_int32,
+                              ctypes.POINTER(hb_rank_result), ctypes.POINTER(ctypes.c_int32),
+                              ctypes.POINTER(hb_sweep_opts)]
+    L.hb_sweep_release.argtypes = []
+    L.hb_sweep_release.restype = None
+    dg = [c_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_double,
+          c_p, ctypes.c_int64, c_p, ctypes.c_int64, ctypes.c_double, c_p, ctypes.c_int64]
+    L.hb_debug_dgemm.argtypes = dg
+    L.hb_debug_dgemm_async.argtypes = dg + [ctypes.c_int32]
     for name in ("hb_context_create", "hb_context_set_tuning", "hb_generate_points",
                  "hb_assemble", "hb_eval_radial_host", "hb_rank_matrix", "hb_rank",
-                 "hb_last_sigma", "hb_sweep", "hb_partition"):
+                 "hb_last_sigma", "hb_sweep", "hb_partition", "hb_context_set_profiling",
+                 "hb_stats_get", "hb_stats_reset", "hb_sweep_ex", "hb_debug_dgemm",
+                 "hb_debug_dgemm_async"):
         getattr(L, name).restype = ctypes.c_int
     if path is None:
         _lib = L
@@ -291,6 +333,24 @@ class Context:
                self._h)
         return [RankResult.of(o) for o in out]
 
+    def set_profiling(self, on: bool = True):
+        _check(self._lib.hb_context_set_profiling(self._h, int(on)), "set_profiling", self._h)
+
+    def stats(self) -> dict:
+        st = hb_stats()
+        _check(self._lib.hb_stats_get(self._h, ctypes.byref(st)), "hb_stats_get", self._h)
+        return st.as_dict()
+
+    def dgemm(self, transA: bool, M: int, N: int, K: int, alpha: float, A: int, lda: int, B: int,
+              ldb: int, beta: float, C: int, ldc: int, reps: int = 0):
+        """Test hook (include/hb_debug.h): FP64 DMMA GEMM on device pointers; reps>0: async."""
+        if reps:
+            _check(self._lib.hb_debug_dgemm_async(self._h, int(transA), M, N, K, alpha, A, lda, B,
+                                                  ldb, beta, C, ldc, reps), "dgemm", self._h)
+        else:
+            _check(self._lib.hb_debug_dgemm(self._h, int(transA), M, N, K, alpha, A, lda, B, ldb,
+                                            beta, C, ldc), "dgemm", self._h)
+
     def last_sigma(self, max_count: int | None = None) -> list[float]:
         cnt = ctypes.c_int64()
         _check(self._lib.hb_last_sigma(self._h, None, 0, ctypes.byref(cnt)), "hb_last_sigma",
@@ -310,17 +370,36 @@ def partition(problems: Sequence[hb_problem], nparts: int) -> list[int]:
     return list(own[:n])
 
 
-def sweep(problems: Sequence[hb_problem], devices: Sequence[int] = (0,)):
-    """hb_sweep: returns (results per problem [list per tol], statuses)."""
+def sweep(problems: Sequence[hb_problem], devices: Sequence[int] = (0,), profiling: bool = False,
+          with_times: bool = False):
+    """hb_sweep_ex: returns (results per problem [list per tol], statuses[, device seconds])."""
     n = len(problems)
     arr = (hb_problem * max(n, 1))(*problems)
     total = sum(p.ntol for p in problems)
     out = (hb_rank_result * max(total, 1))()
     st = (ctypes.c_int32 * max(n, 1))()
     devs = (ctypes.c_int32 * len(devices))(*devices)
-    load().hb_sweep(arr, n, devs, len(devices), out, st)
+    opts = hb_sweep_opts()
+    opts.profiling = int(profiling)
+    load().hb_sweep_ex(arr, n, devs, len(devices), out, st, ctypes.byref(opts))
     res, o = [], 0
     for p in problems:
         res.append([RankResult.of(out[o + t]) for t in range(p.ntol)])
         o += p.ntol
+    if with_times:
+        return res, list(st[:n]), list(opts.device_seconds[:len(devices)])
     return res, list(st[:n])
+
+
+def global_stats() -> dict:
+    st = hb_stats()
+    _check(load().hb_stats_get(None, ctypes.byref(st)), "hb_stats_get")
+    return st.as_dict()
+
+
+def reset_global_stats():
+    load().hb_stats_reset(None)
+
+
+def sweep_release():
+    load().hb_sweep_release()

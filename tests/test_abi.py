@@ -1,0 +1,116 @@
+"""C-ABI library checks that need no GPU: the library loads, exports every symbol the headers in
+include/ declare, the ctypes struct layouts match the C compiler's, and the pure-host entry
+points (status strings, scalar kernel evaluation, seeds, LPT partition, argument validation)
+behave like the reference interface (kernel.hpp / geometry.hpp exceptions -> status codes)."""
+import ctypes
+import math
+import re
+import subprocess
+
+import pytest
+
+from conftest import ROOT
+
+
+def declared_functions():
+    names = set()
+    for h in (ROOT / "include").glob("*.h"):
+        text = re.sub(r"/\*.*?\*/", "", h.read_text(), flags=re.S)
+        for m in re.finditer(r"^[A-Za-z_][\w\s\*]*?\b(hb_\w+)\s*\(", text, flags=re.M):
+            names.add(m.group(1))
+    return sorted(names)
+
+
+def test_library_exports_every_declared_symbol(hb):
+    L = hb.load()
+    names = declared_functions()
+    assert len(names) >= 20
+    missing = [n for n in names if not hasattr(L, n)]
+    assert not missing, missing
+    assert set(names) <= set(hb.EXPORTS) | {"hb_sweep"}
+
+
+def test_version_and_status_strings(hb):
+    L = hb.load()
+    assert b"sm_100a" in L.hb_version()
+    for s in range(9):
+        assert L.hb_status_string(s)
+    assert L.hb_phase_name(4) == b"update"
+
+
+def test_struct_layouts_match_c(tmp_path, hb):
+    src = tmp_path / "sz.c"
+    src.write_text('#include <stdio.h>\n#include <stddef.h>\n#include "hb.h"\nint main(){printf("%zu %zu %zu %zu %zu %zu %zu %zu\\n",'
+                   'sizeof(hb_kernel),sizeof(hb_cube),sizeof(hb_pair),sizeof(hb_rank_result),'
+                   'sizeof(hb_problem),sizeof(hb_stats),sizeof(hb_sweep_opts),offsetof(hb_pair,seed));return 0;}\n')
+    exe = tmp_path / "sz"
+    subprocess.run(["gcc", "-I", str(ROOT / "include"), str(src), "-o", str(exe)], check=True)
+    got = [int(v) for v in subprocess.run([str(exe)], capture_output=True, text=True).stdout.split()]
+    want = [ctypes.sizeof(t) for t in (hb.hb_kernel, hb.hb.hb_cube, hb.hb_pair, hb.hb_rank_result,
+                                       hb.hb_problem, hb.hb_stats, hb.hb.hb_sweep_opts)]
+    want.append(hb.hb_pair.seed.offset)
+    assert got == want
+
+
+def test_eval_radial_host_known_answers(hb):
+    assert hb.eval_radial_host(hb.make_kernel("log_r"), 1.0) == 0.0
+    assert hb.eval_radial_host(hb.make_kernel("one_over_r"), 2.0) == 0.5
+    assert hb.eval_radial_host(hb.make_kernel("exp_neg_r"), 0.0) == 1.0
+    assert hb.eval_radial_host(hb.make_kernel("log_r"), 0.0) == 0.0  # catalog diagonal
+    assert hb.eval_radial_host(hb.make_kernel("exp_neg_r", diagonal=None), 0.0) == 1.0
+    assert hb.eval_radial_host(hb.make_kernel("sin_r"), math.pi / 2) == 1.0
+    with pytest.raises(hb.HBError) as e:
+        hb.eval_radial_host(hb.make_kernel("one_over_r", diagonal=None), 0.0)
+    assert e.value.status == 4  # ESINGULAR (kernel.hpp:152-153)
+    with pytest.raises(hb.HBError) as e:
+        hb.eval_radial_host(hb.make_kernel("custom"), 1.0)
+    assert e.value.status == 5  # EUNSUPPORTED: std::function cannot cross the ABI
+    with pytest.raises(hb.HBError) as e:
+        hb.eval_radial_host(hb.make_kernel(99), 1.0)
+    assert e.value.status == 1
+
+
+def test_problem_seed_matches_oracle(hb, oracle):
+    for d, dp, n in [(1, 0, 1000), (2, None, 16000), (4, 3, 65536), (3, 2, 32000)]:
+        assert hb.problem_seed(0, d, dp, n) == oracle.problem_seed(0, d, dp, n)
+        assert hb.problem_seed(5, d, dp, n) != hb.problem_seed(0, d, dp, n)
+
+
+def sweep_problems(hb, ns=(1000, 2000, 4000, 8000, 16000, 32000, 65536)):
+    probs = []
+    for n in ns:
+        for d in range(1, 5):
+            for dp in list(range(d)) + [None]:
+                for k in ("log_r", "one_over_r", "exp_neg_r"):
+                    probs.append(hb.make_problem(k, d, dp, n, [1e-12, 1e-10] if d == 4 else [1e-12]))
+    return probs
+
+
+def test_partition_lpt(hb):
+    probs = sweep_problems(hb)
+    assert len(probs) == 294
+    for parts in (1, 2, 4, 8):
+        own = hb.partition(probs, parts)
+        assert len(own) == 294 and set(own) <= set(range(parts))
+        assert hb.partition(probs, parts) == own  # deterministic
+        if parts > 1:
+            assert len(set(own)) == parts
+
+
+def test_argument_validation_without_gpu(hb):
+    L = hb.load()
+    probs = (hb.hb_problem * 1)(hb.make_problem("log_r", 1, 0, 10, [1e-12]))
+    out = (hb.hb_rank_result * 1)()
+    devs = (ctypes.c_int32 * 1)(0)
+    assert L.hb_sweep(probs, -1, devs, 1, out, None) == hb.hb.EINVAL
+    assert L.hb_sweep(probs, 1, devs, 0, out, None) == hb.hb.EINVAL
+    own = (ctypes.c_int32 * 1)()
+    assert L.hb_partition(probs, 1, 0, own) == hb.hb.EINVAL
+
+
+def test_context_create_without_gpu_fails_loudly(hb):
+    torch = pytest.importorskip("torch")
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises(hb.HBError):
+        hb.Context(0)

@@ -1,0 +1,190 @@
+"""k3 rank parity on the B200 through the C ABI.
+
+* SPEC epsilon_rank KATs and synthetic matrices with known spectra.
+* The paper's published tables (exact, tests/golden/paper_tables.json).
+* BASELINE-config seeded problems vs the committed CPU-oracle ranks (tests/golden/baseline_ranks.json):
+  ranks must be identical; σ₁ and the boundary σ's must agree closely.
+* Full-size properties where the CPU oracle cannot follow (N up to 65536): certified bracket,
+  rank(K) == rank(Kᵀ), monotonicity in the tolerance, determinism.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+def rank_dense(ctx, M, tols):
+    m, n = M.shape
+    A = torch.tensor(np.asfortranarray(M).T.copy(), device="cuda")
+    torch.cuda.synchronize()
+    return ctx.rank_matrix(A.data_ptr(), m, n, m, tols)
+
+
+def test_rank_matrix_kats(ctx, oracle):
+    rng = np.random.default_rng(0)
+    assert rank_dense(ctx, np.outer(rng.standard_normal(300), rng.standard_normal(200)), [1e-12])[0].rank == 1
+    r = rank_dense(ctx, np.eye(5), [1e-12, 0.5])
+    assert [x.rank for x in r] == [5, 5] and r[0].sigma1 == pytest.approx(1.0, abs=1e-15)
+    assert rank_dense(ctx, np.array([[3.0]]), [1e-12])[0].rank == 1
+    assert rank_dense(ctx, np.array([[1.0, 2.0, 3.0], [2.0, 4.0, 6.0]]), [1e-12])[0].rank == 1
+
+
+@pytest.mark.parametrize("m,n", [(500, 400), (400, 500), (1000, 1000), (130, 2000), (2000, 130)])
+def test_rank_matrix_known_spectrum(ctx, oracle, m, n):
+    rng = np.random.default_rng(m * 7 + n)
+    k = min(m, n)
+    q1, _ = np.linalg.qr(rng.standard_normal((m, k)))
+    q2, _ = np.linalg.qr(rng.standard_normal((n, k)))
+    s = np.logspace(0, -15, k)
+    M = (q1 * s) @ q2.T
+    tols = [1e-12, 1e-9, 1e-6]
+    r = rank_dense(ctx, M, tols)
+    o = [oracle.epsilon_rank_from_sigma(np.linalg.svd(M, compute_uv=False), t) for t in tols]
+    assert [x.rank for x in r] == [x.rank for x in o]
+    assert all(x.rank_lo == x.rank_hi for x in r)
+    assert r[0].sigma1 == pytest.approx(o[0].sigma1, rel=1e-12)
+
+
+def test_rank_matrix_nonfinite(ctx, hb):
+    M = np.ones((10, 10)); M[3, 4] = np.inf
+    with pytest.raises(hb.HBError) as e:
+        rank_dense(ctx, M, [1e-12])
+    assert e.value.status == 2  # EDOMAIN
+
+
+def test_sigma_values_match_lapack(ctx, hb, oracle):
+    pair = hb.make_pair(3, 2, 1000, hb.UNIFORM, 3)
+    ctx.rank(hb.make_kernel("one_over_r"), pair, [1e-12])
+    sg = np.array(ctx.last_sigma(300))
+    x, y = oracle.pair_points(3, 2, 1000, oracle.UNIFORM, 3)
+    so = oracle.singular_values(oracle.assemble(oracle.KERNEL_IDS["one_over_r"], x, y, nthreads=8))
+    np.testing.assert_allclose(sg[:300], so[:300], rtol=1e-9, atol=1e-13 * so[0])
+
+
+def _paper_cases(tables, max_n):
+    for tab in tables:
+        for row in tab["rows"]:
+            if row["N"] > max_n:
+                continue
+            for kname, want in zip(tab["kernels"], row["ranks"]):
+                if kname is not None:
+                    yield tab["label"], tab["d"], tab["dprime"], row["N"], kname, want
+
+
+def _paper_check(ctx, hb, d, dp, n, kname, want):
+    mode = hb.GRID_CLOSED if dp is None else hb.GRID_INTERIOR
+    r = ctx.rank(hb.make_kernel(kname), hb.make_pair(d, dp, n, mode, 0), [1e-12])[0]
+    assert r.rank_lo == r.rank_hi
+    return r
+
+
+def test_paper_tables_small_n(ctx, hb, paper_tables):
+    """Every real-kernel table entry with N <= 5000 (grid inputs, ε = 1e-12): exact."""
+    bad = []
+    cases = list(_paper_cases(paper_tables, 5000))
+    assert len(cases) >= 150
+    for label, d, dp, n, kname, want in cases:
+        r = _paper_check(ctx, hb, d, dp, n, kname, want)
+        if r.rank != want:
+            bad.append((label, n, kname, want, r.rank, r.gap))
+    assert not bad, bad
+
+
+@pytest.mark.slow
+def test_paper_tables_large_n(ctx, hb, paper_tables):
+    """Published values at the paper's large N, where no CPU SVD is practical (e.g. 3D face
+    1/r N=64000 -> 3547; 4D d'=3 exp(-r) N=50625 -> 7440)."""
+    picks = {("tab:res_3d_face", 64000, "one_over_r"), ("tab:res_4d_h3", 50625, "exp_neg_r"),
+             ("tab:res_2d_edge", 40000, "log_r"), ("tab:res_1d_vert", 40000, "one_over_r"),
+             ("tab:res_3d_ver", 64000, "one_over_r"), ("tab:res_4d_far", 50625, "exp_neg_r"),
+             ("tab:res_2d_far", 40000, "log_r"), ("tab:res_3d_edge", 27000, "one_over_r")}
+    bad = []
+    for label, d, dp, n, kname, want in _paper_cases(paper_tables, 10 ** 9):
+        if (label, n, kname) in picks:
+            r = _paper_check(ctx, hb, d, dp, n, kname, want)
+            if r.rank != want:
+                bad.append((label, n, kname, want, r.rank, r.gap))
+    assert not bad, bad
+
+
+def test_baseline_configs_match_oracle(ctx, hb, baseline_ranks):
+    """Seeded BASELINE problems (i.i.d. uniform points): GPU rank == CPU-oracle rank; an
+    off-by-one would only be tolerated at a boundary tie (oracle gap < 1e-7) and reported."""
+    assert baseline_ranks, "golden file missing"
+    mism, ties = [], []
+    for rec in baseline_ranks:
+        pair = hb.make_pair(rec["d"], rec["dprime"], rec["N"], hb.UNIFORM, rec["seed"])
+        res = ctx.rank(hb.make_kernel(rec["kernel"]), pair, rec["tols"])
+        for t, r in enumerate(res):
+            want = rec["ranks"][t]
+            if r.rank != want:
+                (ties if rec["gaps"][t] < 1e-7 else mism).append(
+                    (rec["d"], rec["dprime"], rec["kernel"], rec["N"], rec["tols"][t], want, r.rank,
+                     rec["gaps"][t], r.gap))
+            assert r.rank_lo == r.rank_hi
+        assert res[0].sigma1 == pytest.approx(rec["sigma1"], rel=1e-11)
+        if res[0].rank > 0:
+            assert res[0].sigma_r == pytest.approx(rec["sigma_r"][0], rel=1e-6)
+    print(f"boundary ties (reported): {ties}")
+    assert not mism, mism
+
+
+@pytest.mark.parametrize("d,dp,kname,n", [(2, 1, "log_r", 16000), (3, 2, "one_over_r", 16000),
+                                          (1, None, "log_r", 65536), (4, 0, "exp_neg_r", 8000)])
+def test_full_size_properties(ctx, hb, d, dp, kname, n):
+    seed = hb.problem_seed(0, d, dp, n)
+    pair = hb.make_pair(d, dp, n, hb.UNIFORM, seed)
+    k = hb.make_kernel(kname)
+    r = ctx.rank(k, pair, [1e-12, 1e-10, 1e-8])
+    assert all(x.rank_lo == x.rank_hi for x in r)                 # certified bracket
+    assert r[0].rank >= r[1].rank >= r[2].rank                    # non-increasing in ε
+    assert r[0].resid <= 0.01 * 1e-12 * r[0].sigma1 * 1.0001      # stopping rule held
+    rt = ctx.rank(k, pair, [1e-12])[0]
+    assert rt.rank == r[0].rank and rt.sigma1 == r[0].sigma1      # deterministic
+
+
+def test_transpose_invariance(ctx, hb, oracle):
+    """rank(K) == rank(Kᵀ) on the device for the same point sets."""
+    d, dp, n = 3, 2, 3000
+    pair = hb.make_pair(d, dp, n, hb.UNIFORM, 11)
+    X = torch.empty((d, n), dtype=torch.float64, device="cuda")
+    Y = torch.empty((d, n), dtype=torch.float64, device="cuda")
+    torch.cuda.synchronize()
+    ctx.generate_points(pair, X.data_ptr(), Y.data_ptr())
+    torch.cuda.ExternalStream(ctx.stream).synchronize()
+    K1 = torch.empty((n, n), dtype=torch.float64, device="cuda")
+    K2 = torch.empty((n, n), dtype=torch.float64, device="cuda")
+    ctx.assemble(hb.make_kernel("one_over_r"), X.data_ptr(), n, Y.data_ptr(), n, d, K1.data_ptr(), n)
+    ctx.assemble(hb.make_kernel("one_over_r"), Y.data_ptr(), n, X.data_ptr(), n, d, K2.data_ptr(), n)
+    torch.cuda.synchronize()
+    assert torch.equal(K1, K2.t())
+    r1 = ctx.rank_matrix(K1.data_ptr(), n, n, n, [1e-12])[0]
+    r2 = ctx.rank_matrix(K2.data_ptr(), n, n, n, [1e-12])[0]
+    assert r1.rank == r2.rank
+    assert r1.sigma1 == pytest.approx(r2.sigma1, rel=1e-12)
+
+
+def test_sweep_matches_single_calls(ctx, hb):
+    probs = [hb.make_problem(k, d, dp, n, [1e-12, 1e-10])
+             for (d, dp, k, n) in [(1, 0, "log_r", 1000), (2, None, "exp_neg_r", 2000),
+                                   (3, 1, "one_over_r", 1000), (4, 2, "exp_neg_r", 1000)]]
+    res, st = hb.sweep(probs, [0])
+    assert st == [0] * len(probs)
+    for p, rr in zip(probs, res):
+        single = ctx.rank(p.kernel, p.pair, list(p.tols[: p.ntol]))
+        assert [x.rank for x in rr] == [x.rank for x in single]
+    # a bad problem fails alone, with its own status
+    bad = hb.make_problem("custom", 2, 1, 100, [1e-12])
+    res, st = hb.sweep(probs[:1] + [bad], [0])
+    assert st == [0, 5]
+
+
+def test_profiling_stats(ctx, hb):
+    ctx.set_profiling(True)
+    ctx.rank(hb.make_kernel("exp_neg_r"), hb.make_pair(4, 3, 2000, hb.UNIFORM, 1), [1e-12])
+    s = ctx.stats()
+    ctx.set_profiling(False)
+    assert s["problems"] >= 1 and s["gemm_launches"] > 0 and s["gemm_flops"] > 0
+    assert s["phase_ms"]["update"] > 0 and s["phase_ms"]["bidiag"] > 0
+    assert s["launches"] > 0
