@@ -106,4 +106,20 @@ __device__ __forceinline__ double block_sum(double v, double* smem) {
   return t;
 }
 
+// Sum of n values base[h*stride] (h < n) over the whole block, fixed order (deterministic).
+__device__ __forceinline__ double block_sum_strided(const double* base, int n, int64_t stride,
+                                                    double* smem) {
+  double v = 0.0;
+  for (int h = threadIdx.x; h < n; h += blockDim.x) v += base[(int64_t)h * stride];
+  return block_sum(v, smem);
+}
+
+// Warp-wide sum of n values base[h*stride]; result in every lane, fixed order.
+__device__ __forceinline__ double warp_sum_strided(const double* base, int n, int64_t stride) {
+  const int lane = threadIdx.x & 31;
+  double v = 0.0;
+  for (int h = lane; h < n; h += 32) v += base[(int64_t)h * stride];
+  return warp_sum(v);
+}
+
 }  // namespace hb

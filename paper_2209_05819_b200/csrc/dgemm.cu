@@ -84,6 +84,14 @@ __global__ void __launch_bounds__(256, 1) dgemm_kernel(GemmParams p) {
   const int64_t kbeg = (int64_t)blockIdx.z * p.kchunk;
   const int64_t kend = min(p.K, kbeg + p.kchunk);
   const int nk = kend > kbeg ? (int)((kend - kbeg + BK - 1) / BK) : 0;
+  if (p.beta != 0.0 && !p.partial) {
+    // warm L2 with this CTA's C tile while the main loop runs (128-byte lines)
+    for (int v = tid; v < BN * (BM / 16); v += 256) {
+      const int64_t m = m0 + (v % (BM / 16)) * 16, n = n0 + v / (BM / 16);
+      if (m < p.M && n < p.N)
+        asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p.C + m + n * p.ldc));
+    }
+  }
 
   auto load_tile = [&](int kt, int stage) {
     const int64_t k0 = kbeg + (int64_t)kt * BK;
@@ -187,30 +195,89 @@ __global__ void __launch_bounds__(256, 1) dgemm_kernel(GemmParams p) {
   }
   cp_wait<0>();
 
+  if (p.partial) {
+#pragma unroll
+    for (int i = 0; i < WM; ++i) {
+      const int64_t m = m0 + (wm * WM + i) * 8 + ar;
+      if (m >= p.M) continue;
+#pragma unroll
+      for (int j = 0; j < WN; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int64_t n = n0 + (wn * WN + j) * 8 + 2 * ac + h;
+          if (n < p.N) p.partial[(int64_t)blockIdx.z * p.M * p.N + m + n * p.M] = p.alpha * acc[i][j][h];
+        }
+    }
+    return;
+  }
+  // Epilogue: stage the accumulator tile through shared memory (the operand buffers are free
+  // now), half a tile of columns at a time, then read-modify-write C with 16-byte accesses and
+  // all loads of a thread in flight together.  LDC = BM + 2 keeps the fragment stores
+  // bank-conflict free.
+  constexpr int LDC = BM + 2;
+  constexpr int HALF = BN / 2;
+  static_assert(HALF * LDC <= STAGES * (C_::A_ELEMS + C_::B_ELEMS), "epilogue tile too large");
+  double* Cs = smem;
   double fro = 0.0;
+  const bool cvec = ((p.ldc & 1) == 0) && ((reinterpret_cast<uintptr_t>(p.C) & 15) == 0);
 #pragma unroll
-  for (int i = 0; i < WM; ++i) {
-    const int64_t m = m0 + (wm * WM + i) * 8 + ar;
-    if (m >= p.M) continue;
+  for (int half = 0; half < 2; ++half) {
+    __syncthreads();
 #pragma unroll
-    for (int j = 0; j < WN; ++j) {
+    for (int i = 0; i < WM; ++i)
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int64_t n = n0 + (wn * WN + j) * 8 + 2 * ac + h;
-        if (n >= p.N) continue;
-        const double v = p.alpha * acc[i][j][h];
-        if (p.partial) {
-          p.partial[(int64_t)blockIdx.z * p.M * p.N + m + n * p.M] = v;
-        } else {
-          double* c = p.C + m + n * p.ldc;
-          const double out = p.beta == 0.0 ? v : v + p.beta * *c;
-          *c = out;
-          if (m >= p.fro_row0) fro += out * out;
+      for (int j = 0; j < WN; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int nl = (wn * WN + j) * 8 + 2 * ac + h - half * HALF;
+          if (nl >= 0 && nl < HALF) Cs[nl * LDC + (wm * WM + i) * 8 + ar] = acc[i][j][h];
+        }
+    __syncthreads();
+    constexpr int VPC = BM / 2;                 // 2-double vectors per column
+    constexpr int PER = VPC * HALF / 256;       // vectors per thread
+    double2 cv[PER];
+    if (p.beta != 0.0) {
+#pragma unroll
+      for (int t = 0; t < PER; ++t) {
+        const int v = tid + t * 256;
+        const int ml = (v % VPC) * 2, nl = v / VPC;
+        const int64_t m = m0 + ml, n = n0 + half * HALF + nl;
+        cv[t] = make_double2(0.0, 0.0);
+        if (n < p.N) {
+          const double* c = p.C + m + n * p.ldc;
+          if (cvec && m + 1 < p.M) cv[t] = *reinterpret_cast<const double2*>(c);
+          else {
+            if (m < p.M) cv[t].x = c[0];
+            if (m + 1 < p.M) cv[t].y = c[1];
+          }
         }
       }
     }
+#pragma unroll
+    for (int t = 0; t < PER; ++t) {
+      const int v = tid + t * 256;
+      const int ml = (v % VPC) * 2, nl = v / VPC;
+      const int64_t m = m0 + ml, n = n0 + half * HALF + nl;
+      if (n >= p.N || m >= p.M) continue;
+      double2 o;
+      o.x = p.alpha * Cs[nl * LDC + ml];
+      o.y = p.alpha * Cs[nl * LDC + ml + 1];
+      if (p.beta != 0.0) {
+        o.x += p.beta * cv[t].x;
+        o.y += p.beta * cv[t].y;
+      }
+      double* c = p.C + m + n * p.ldc;
+      if (cvec && m + 1 < p.M) {
+        *reinterpret_cast<double2*>(c) = o;
+      } else {
+        c[0] = o.x;
+        if (m + 1 < p.M) c[1] = o.y;
+      }
+      if (m >= p.fro_row0) fro += o.x * o.x;
+      if (m + 1 >= p.fro_row0 && m + 1 < p.M) fro += o.y * o.y;
+    }
   }
-  if (p.fro && !p.partial) {
+  if (p.fro) {
     const double s = block_sum(fro, red);
     if (tid == 0) p.fro[(int64_t)blockIdx.y * gridDim.x + blockIdx.x] = s;
   }

@@ -96,22 +96,40 @@ __global__ void __launch_bounds__(256) sketch_cpqr_kernel(SketchParams p) {
 
   int c = 0;
   for (; c < p.b_req; ++c) {
-    // global argmax + total remaining sketch mass (fixed order -> identical in every CTA)
-    if (tid == 0) {
+    // global argmax + total remaining sketch mass (block-parallel, fixed order -> identical in
+    // every CTA)
+    {
+      const double* sl = p.slots + (size_t)(c & 1) * G * 3;
       double b0 = -1.0, s0 = 0.0;
       int i0 = INT_MAX;
-      const double* sl = p.slots + (size_t)(c & 1) * G * 3;
-      for (int h = 0; h < G; ++h) {
+      for (int h = tid; h < G; h += 256) {
         if (better(sl[3 * h], (int)sl[3 * h + 1], b0, i0)) { b0 = sl[3 * h]; i0 = (int)sl[3 * h + 1]; }
         s0 += sl[3 * h + 2];
       }
-      const double est = c < ell ? s0 / (double)(ell - c) : 0.0;
-      if (g == 0) p.out_est[c] = est;
-      int stop = 0;
-      if (!(b0 > 0.0) || c >= ell) stop = 1;
-      else if (c >= p.b_min && (c % 8) == 0 && est <= p.stop_fro2) stop = 1;
-      sh_stop = stop;
-      sh_piv = i0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, b0, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, i0, o);
+        if (better(ob, oi, b0, i0)) { b0 = ob; i0 = oi; }
+      }
+      s0 = warp_sum(s0);
+      if (lane == 0) { wbest[warp] = b0; wbi[warp] = i0; wsum[warp] = s0; }
+      __syncthreads();
+      if (tid == 0) {
+        double bb = -1.0, ss = 0.0;
+        int ii = INT_MAX;
+        for (int w = 0; w < 8; ++w) {
+          if (better(wbest[w], wbi[w], bb, ii)) { bb = wbest[w]; ii = wbi[w]; }
+          ss += wsum[w];
+        }
+        const double est = c < ell ? ss / (double)(ell - c) : 0.0;
+        if (g == 0) p.out_est[c] = est;
+        int stop = 0;
+        if (!(bb > 0.0) || c >= ell) stop = 1;
+        else if (c >= p.b_min && (c % 8) == 0 && est <= p.stop_fro2) stop = 1;
+        sh_stop = stop;
+        sh_piv = ii;
+      }
     }
     __syncthreads();
     if (sh_stop) break;
@@ -240,6 +258,7 @@ __global__ void __launch_bounds__(256) panel_qr_kernel(PanelParams p) {
   double* vs = psm;
   double* ws = psm + chunk;
   __shared__ double sh[4];
+  __shared__ double red[32];
   double* P = p.P;
   const int64_t ld = p.ld;
 
@@ -255,10 +274,13 @@ __global__ void __launch_bounds__(256) panel_qr_kernel(PanelParams p) {
   }
   grid_sync(p.bar);
 
-  for (int c = 0; c < b; ++c) {
-    if (tid == 0) {
-      double s = 0.0;
-      for (int h = 0; h < G; ++h) s += p.nslot[h];
+  // reflectors for the first min(b, mp) columns (a wide panel, mp < b, occurs in the block LQ of
+  // the band reduction); the remaining columns are only transformed
+  const int nref = (int)min((int64_t)b, p.mp);
+  for (int c = 0; c < nref; ++c) {
+    {
+      const double s = block_sum_strided(p.nslot, G, 1, red);
+      if (tid == 0) {
       const double alpha = P[c + (int64_t)c * ld];
       double tau = 0.0, scal = 0.0, beta = alpha;
       if (s > 0.0) {
@@ -267,6 +289,7 @@ __global__ void __launch_bounds__(256) panel_qr_kernel(PanelParams p) {
         scal = 1.0 / (alpha - beta);
       }
       sh[0] = tau; sh[1] = scal; sh[2] = beta;
+      }
     }
     __syncthreads();
     const double tau = sh[0], scal = sh[1];
@@ -292,10 +315,9 @@ __global__ void __launch_bounds__(256) panel_qr_kernel(PanelParams p) {
       if (lane == 0) p.wslot[(size_t)g * b + q] = s;
     }
     grid_sync(p.bar);
-    for (int q = c + 1 + tid; q < b; q += 256) {
-      double s = 0.0;
-      for (int h = 0; h < G; ++h) s += p.wslot[(size_t)h * b + q];
-      ws[q] = s * tau;
+    for (int q = c + 1 + warp; q < b; q += 8) {
+      const double s = warp_sum_strided(p.wslot + q, G, b);
+      if (lane == 0) ws[q] = s * tau;
     }
     __syncthreads();
     for (int q = c + 1 + warp; q < b; q += 8) {
@@ -317,12 +339,15 @@ __global__ void __launch_bounds__(256) panel_qr_kernel(PanelParams p) {
     if (g == 0 && tid == 0) p.tau[c] = tau;
     grid_sync(p.bar);
   }
-  // explicit V (unit diagonal, zeros above)
+  // explicit V (unit diagonal, zeros above; zero columns beyond the last reflector)
   for (int q = warp; q < b; q += 8) {
     const double* colq = P + (int64_t)q * ld;
     double* vq = p.V + (int64_t)q * p.ldv;
-    for (int64_t i = r0 + lane; i < r1; i += 32) vq[i] = i > q ? colq[i] : (i == q ? 1.0 : 0.0);
+    for (int64_t i = r0 + lane; i < r1; i += 32)
+      vq[i] = q >= nref ? 0.0 : (i > q ? colq[i] : (i == q ? 1.0 : 0.0));
   }
+  if (g == 0)
+    for (int q = nref + tid; q < b; q += 256) p.tau[q] = 0.0;
 }
 
 // T of the compact-WY form from S = VᵀV and τ (LAPACK dlarft, forward/columnwise).
@@ -380,17 +405,18 @@ __global__ void __launch_bounds__(256) power_sigma1_kernel(PowerParams p) {
   double best = 0.0;
   for (int it = 0; it <= p.iters; ++it) {
     // x from previous partials (it == 0: ones)
-    if (tid < b) {
-      double s = 0.0;
-      if (it == 0) s = 1.0;
-      else
-        for (int h = 0; h < G; ++h) s += p.slots[(size_t)((it - 1) & 1) * G * (b + 1) + (size_t)h * (b + 1) + tid];
-      x[tid] = s;
-    }
-    if (tid == 0 && it > 0) {
-      double s = 0.0;
-      for (int h = 0; h < G; ++h) s += p.slots[(size_t)((it - 1) & 1) * G * (b + 1) + (size_t)h * (b + 1) + b];
-      best = fmax(best, sqrt(s));  // ||R^T x_hat|| of the previous iterate
+    {
+      const double* prev = p.slots + (size_t)((it - 1) & 1) * G * (b + 1);
+      for (int i = warp; i <= b; i += 8) {
+        const double s = it == 0 ? (i < b ? 1.0 : 0.0) : warp_sum_strided(prev + i, G, b + 1);
+        if (lane == 0) {
+          if (i < b) x[i] = s;
+          else ysum[0] = s;
+        }
+      }
+      __syncthreads();
+      if (tid == 0 && it > 0) best = fmax(best, sqrt(ysum[0]));  // ||R^T x_hat|| of the previous iterate
+      __syncthreads();
     }
     __syncthreads();
     if (tid == 0) {

@@ -87,6 +87,12 @@ struct SigmaAnswer {
   double sigma1, sigma_p, sigma_p1;
   int rank_lo, rank_hi;
 };
+__global__ void transpose_kernel(const double* src, int64_t lds, int64_t rows, int64_t cols,
+                                 double* dst, int64_t ldd);
+__global__ void write_lower_from_R(const double* R, int64_t ldr, int b, int nc, double* M, int64_t ldm);
+__global__ void band_extract_kernel(const double* M, int64_t ldm, int64_t k, int nb, double* Bd);
+__global__ void band_bidiag_out(const double* Bd, int64_t k, int nb, double* d, double* e);
+__global__ void bulge_chase_kernel(double* Bd, int64_t k, int nb, int* prog);
 __global__ void sigma_queries_kernel(const double* d, const double* e, int64_t k,
                                      const SigmaQuery* q, int nq, SigmaAnswer* out);
 __global__ void sigma_all_kernel(const double* d, const double* e, int64_t k, double sigma_max,

@@ -26,6 +26,7 @@ void coop(void (*kern)(P), int grid, size_t smem, cudaStream_t st, P prm) {
     HB_CUDA(cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem));
   HB_CUDA(cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(256), args, smem, st));
+  launch_counter().fetch_add(1);
 }
 
 int clampi(int64_t v, int lo, int hi) { return (int)std::max<int64_t>(lo, std::min<int64_t>(hi, v)); }
@@ -122,6 +123,73 @@ void sketch(hb_context* c, const double* A, int64_t lda, int64_t m, int64_t n, d
   g.M = kSketchRows; g.N = n; g.K = m; g.alpha = 1.0; g.A = Om; g.lda = kSketchRows;
   g.transA = false; g.B = A; g.ldb = lda; g.beta = 0.0; g.C = Y; g.ldc = kSketchRows;
   Gemm{c}(g);
+}
+
+// Two-stage Golub–Kahan bidiagonalisation of the k x k upper triangle Mk (destroyed):
+// stage 1 dense -> upper band (bandwidth kBand) with DMMA GEMM updates, stage 2 bulge chasing.
+constexpr int kBand = 32;
+
+void two_stage_bidiag(hb_context* c, double* Mk, int64_t ldm, int64_t k, double* d, double* e,
+                      double* V, int64_t ldv, double* tau, double* T) {
+  cudaStream_t st = c->stream;
+  const int64_t ldp = round_up(k, 8);
+  double* P2 = ws<double>(c, B_ST1_P, (size_t)ldp * kBand);
+  double* X = ws<double>(c, B_ST1_X, (size_t)ldp * kBand);
+  double* X2 = ws<double>(c, B_ST1_X2, (size_t)ldp * kBand);
+  double* Vt = ws<double>(c, B_ST1_VT, (size_t)kBand * ldp);
+  Gemm gemm{c};
+  for (int64_t i = 0; i < k; i += kBand) {
+    const int b = (int)std::min<int64_t>(kBand, k - i);
+    panel_and_T(c, Mk + i + i * ldm, ldm, k - i, b, V, ldv, tau, T);
+    if (i + b >= k) break;
+    const int64_t nc = k - i - b;
+    apply_block_reflector(c, V, ldv, T, b, Mk + i + (i + b) * ldm, ldm, k - i, nc, nullptr);
+    // block LQ of the row panel Mk[i:i+b, i+b:k] = QR of its transpose
+    dim3 tb(32, 8);
+    transpose_kernel<<<dim3((unsigned)ceil_div(nc, 32), (unsigned)ceil_div(b, 32)), tb, 0, st>>>(
+        Mk + i + (i + b) * ldm, ldm, b, nc, P2, ldp);
+    HB_LAUNCH_CHECK();
+    panel_and_T(c, P2, ldp, nc, b, V, ldv, tau, T);
+    const int nl = (int)std::min<int64_t>(b, nc);
+    write_lower_from_R<<<nl, kBand, 0, st>>>(P2, ldp, b, nl, Mk + i + (i + b) * ldm, ldm);
+    HB_LAUNCH_CHECK();
+    // trailing rows from the right: M2 <- M2 (I - V T V^T), M2 = Mk[i+b:k, i+b:k]
+    double* M2 = Mk + (i + b) + (i + b) * ldm;
+    GemmArgs g1{};
+    g1.M = nc; g1.N = b; g1.K = nc; g1.alpha = 1.0; g1.A = M2; g1.lda = ldm; g1.B = V; g1.ldb = ldv;
+    g1.beta = 0.0; g1.C = X; g1.ldc = ldp;
+    gemm(g1);
+    GemmArgs g2{};
+    g2.M = nc; g2.N = b; g2.K = b; g2.alpha = 1.0; g2.A = X; g2.lda = ldp; g2.B = T; g2.ldb = b;
+    g2.beta = 0.0; g2.C = X2; g2.ldc = ldp;
+    gemm(g2);
+    transpose_kernel<<<dim3((unsigned)ceil_div(b, 32), (unsigned)ceil_div(nc, 32)), tb, 0, st>>>(
+        V, ldv, nc, b, Vt, b);
+    HB_LAUNCH_CHECK();
+    GemmArgs g3{};
+    g3.M = nc; g3.N = nc; g3.K = b; g3.alpha = -1.0; g3.A = X2; g3.lda = ldp; g3.B = Vt; g3.ldb = b;
+    g3.beta = 1.0; g3.C = M2; g3.ldc = ldm;
+    gemm(g3);
+  }
+  // stage 2: band -> bidiagonal
+  const int W = 3 * kBand + 1;
+  double* Bd = ws<double>(c, B_CERT_B2, (size_t)k * W);
+  band_extract_kernel<<<(unsigned)ceil_div(k * W, 256), 256, 0, st>>>(Mk, ldm, k, kBand, Bd);
+  HB_LAUNCH_CHECK();
+  if (k > 1) {
+    int* prog = ws<int>(c, B_PROG, (size_t)k);
+    HB_CUDA(cudaMemsetAsync(prog, 0, sizeof(int) * k, st));
+    int per_sm = 0;
+    HB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bulge_chase_kernel, 128, 0));
+    const int G = clampi(k - 1, 1, std::max(1, std::min(per_sm, 8)) * c->num_sms);
+    int kb = kBand;
+    int64_t kk = k;
+    void* args[] = {&Bd, &kk, &kb, &prog};
+    HB_CUDA(cudaLaunchCooperativeKernel((const void*)bulge_chase_kernel, dim3(G), dim3(128), args, 0, st));
+    launch_counter().fetch_add(1);
+  }
+  band_bidiag_out<<<(unsigned)ceil_div(k, 256), 256, 0, st>>>(Bd, k, kBand, d, e);
+  HB_LAUNCH_CHECK();
 }
 
 }  // namespace
@@ -298,21 +366,7 @@ void rank_matrix_inplace(hb_context* c, double* A, int64_t m, int64_t n, int64_t
     Phase ph_bd(c, HB_PH_BIDIAG);
     double* d = ws<double>(c, B_D, (size_t)k + 1);
     double* e = ws<double>(c, B_E, (size_t)k + 1);
-    HB_CUDA(cudaMemsetAsync(e, 0, sizeof(double) * (k + 1), st));
-    const int64_t nb = ceil_div(k, 32);
-    const int G = clampi(nb, 1, c->num_sms);
-    const int64_t nown = ceil_div(nb, G);
-    BidiagParams bp{};
-    bp.M = Mk; bp.ld = ldm; bp.k = k; bp.d = d; bp.e = e;
-    bp.wslot = ws<double>(c, B_BW, (size_t)G * k);
-    bp.w = ws<double>(c, B_BV, (size_t)2 * k + 8);
-    bp.v = bp.w + k + 4;
-    bp.nslot = ws<double>(c, B_SLOTS, (size_t)c->num_sms * (kBlockMax + 1) * 2 + 64);
-    bp.scal = scal + 4;
-    bp.bar = barrier(c);
-    const size_t smem = (size_t)nown * 32 * 9 * sizeof(double);
-    HB_REQUIRE(smem <= 200 * 1024, HB_ECAP, "bidiag: k too large");
-    coop(bidiag_kernel, G, smem, st, bp);
+    two_stage_bidiag(c, Mk, ldm, k, d, e, V, ldv, tau, T);
     ph_bd.close();
     Phase ph_bs(c, HB_PH_BISECT);
     SigmaQuery* dq = ws<SigmaQuery>(c, B_QUERY, HB_MAX_TOLS);

@@ -27,6 +27,7 @@ __global__ void __launch_bounds__(256) bidiag_kernel(BidiagParams p) {
   double* u = bsm;                      // [nown*32]
   double* zp = bsm + nown * 32;         // [8][nown*32]
   __shared__ double sh[4];
+  __shared__ double red[32];
 
   auto own_row = [&](int64_t t) { return (g + t * G) * 32; };
 
@@ -45,9 +46,9 @@ __global__ void __launch_bounds__(256) bidiag_kernel(BidiagParams p) {
 
   for (int64_t i = 0; i < k; ++i) {
     // ---- left reflector from column i ----
+    const double s_all = block_sum_strided(p.nslot, G, 1, red);
     if (tid == 0) {
-      double s = 0.0;
-      for (int h = 0; h < G; ++h) s += p.nslot[h];
+      const double s = s_all;
       const double alpha = M[i + i * ld];
       double tau = 0.0, scal = 0.0, beta = alpha;
       if (s > 0.0) {
@@ -82,10 +83,9 @@ __global__ void __launch_bounds__(256) bidiag_kernel(BidiagParams p) {
     }
     grid_sync(p.bar);
     if (i + 1 < k) {
-      for (int64_t q = i + 1 + g + (int64_t)tid * G; q < k; q += (int64_t)G * 256) {
-        double s = 0.0;
-        for (int h = 0; h < G; ++h) s += p.wslot[(size_t)h * k + q];
-        p.w[q] = s * tau_u;
+      for (int64_t q = i + 1 + g + (int64_t)warp * G; q < k; q += (int64_t)G * 8) {
+        const double s = warp_sum_strided(p.wslot + q, G, k);
+        if (lane == 0) p.w[q] = s * tau_u;
       }
     }
     grid_sync(p.bar);
@@ -254,6 +254,206 @@ __global__ void sigma_all_kernel(const double* __restrict__ d, const double* __r
   double pivmin = 1e-290;
   const double ub = sigma_max * (1.0 + 1e-12) + 1e-300;
   out[wid] = kth_largest(d, e, k, wid + 1, 0.0, ub, pivmin);
+}
+
+}  // namespace hb
+
+// ================================================================================================
+// Two-stage bidiagonalisation (certification of large k).
+// Stage 1 (host-driven, rank.cu): dense k x k -> upper band of bandwidth nb by alternating block
+// QR (column panel, from the left) and block LQ (row panel, from the right), all trailing updates
+// as DMMA GEMMs.  Stage 2 (bulge_chase_kernel): band -> upper bidiagonal by Householder bulge
+// chasing (one sweep per row; tasks R/L alternate, each annihilating one row/column segment of
+// length <= nb and pushing the bulge nb further down).  The algorithm and the inter-sweep lag
+// (sweep s task t may start once sweep s-1 finished task t+3) were pinned with the numpy
+// prototype tools/proto_bulge.py.  Band storage: row-major, offsets -nb..2nb around the
+// diagonal (W = 3nb + 1 per row); all nonzeros stay within offsets [-(nb-1), 2nb-1].
+// ================================================================================================
+namespace hb {
+
+__global__ void transpose_kernel(const double* __restrict__ src, int64_t lds, int64_t rows,
+                                 int64_t cols, double* __restrict__ dst, int64_t ldd) {
+  __shared__ double tile[32][33];
+  const int64_t r0 = (int64_t)blockIdx.y * 32, c0 = (int64_t)blockIdx.x * 32;
+  for (int y = threadIdx.y; y < 32; y += blockDim.y) {
+    const int64_t c = c0 + y, r = r0 + threadIdx.x;
+    tile[y][threadIdx.x] = (r < rows && c < cols) ? src[r + c * lds] : 0.0;
+  }
+  __syncthreads();
+  for (int y = threadIdx.y; y < 32; y += blockDim.y) {
+    const int64_t r = r0 + y, c = c0 + threadIdx.x;  // dst(c, r) = src(r, c)
+    if (r < rows && c < cols) dst[c + r * ldd] = tile[threadIdx.x][y];
+  }
+}
+
+// M[i + r, j0 + c] = R[c, r] for c <= r (r < b, c < nc): the LQ factor L = R_Pᵀ of a row panel.
+__global__ void write_lower_from_R(const double* __restrict__ R, int64_t ldr, int b, int nc,
+                                   double* __restrict__ M, int64_t ldm) {
+  const int r = threadIdx.x, c = blockIdx.x;
+  if (r < b && c < nc && c <= r) M[r + (int64_t)c * ldm] = R[c + (int64_t)r * ldr];
+}
+
+// Band (offsets 0..nb of the upper-band matrix M) -> compact storage Bd (offsets -nb..2nb, zeroed
+// elsewhere).
+__global__ void band_extract_kernel(const double* __restrict__ M, int64_t ldm, int64_t k, int nb,
+                                    double* __restrict__ Bd) {
+  const int W = 3 * nb + 1;
+  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= k * W) return;
+  const int64_t r = idx / W;
+  const int o = (int)(idx % W) - nb;
+  const int64_t c = r + o;
+  Bd[idx] = (o >= 0 && o <= nb && c < k) ? M[r + c * ldm] : 0.0;
+}
+
+__global__ void band_bidiag_out(const double* __restrict__ Bd, int64_t k, int nb,
+                                double* __restrict__ d, double* __restrict__ e) {
+  const int W = 3 * nb + 1;
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= k) return;
+  d[i] = Bd[i * W + nb];
+  e[i] = i + 1 < k ? Bd[i * W + nb + 1] : 0.0;
+}
+
+struct ChaseTask {
+  bool right;   // R: reflector over columns, applied to rows; L: over rows, applied to columns
+  int64_t idx;  // row (R) / column (L) whose segment is annihilated
+  int64_t lo, hi;    // reflector span (columns for R, rows for L)
+  int64_t alo, ahi;  // application range (rows for R, columns for L)
+};
+
+// t-th task of sweep s (tools/proto_bulge.py tasks_of_sweep); returns false past the end.
+__device__ bool chase_task(int64_t s, int t, int64_t k, int nb, ChaseTask* tk) {
+  const int q = t >> 1;
+  const int64_t c0 = s + 1 + (int64_t)q * nb;
+  if (c0 > k - 1) return false;
+  const int64_t c1 = min(c0 + nb - 1, k - 1);
+  if ((t & 1) == 0) {
+    if (!(c1 > c0 || q == 0)) return false;
+    tk->right = true;
+    tk->idx = q == 0 ? s : s + 1 + (int64_t)(q - 1) * nb;
+    tk->lo = c0; tk->hi = c1;
+    tk->alo = tk->idx; tk->ahi = min(k - 1, c1 + nb - 1);
+    return true;
+  }
+  if (!(c1 > c0)) return false;
+  tk->right = false;
+  tk->idx = c0;
+  tk->lo = c0; tk->hi = c1;
+  tk->alo = c0; tk->ahi = min(k - 1, c1 + nb);
+  return true;
+}
+
+__device__ int chase_ntasks(int64_t s, int64_t k, int nb) {
+  int t = 0;
+  ChaseTask tk;
+  while (chase_task(s, t, k, nb, &tk)) ++t;
+  return t;
+}
+
+__device__ __forceinline__ int64_t band_off(int64_t r, int64_t c, int nb, int W) {
+  return r * W + (c - r + nb);
+}
+__device__ __forceinline__ bool band_in(int64_t r, int64_t c, int nb) {
+  const int64_t o = c - r;
+  return o >= -nb && o <= 2 * nb;
+}
+
+__global__ void __launch_bounds__(128) bulge_chase_kernel(double* __restrict__ Bd, int64_t k, int nb,
+                                                          int* __restrict__ prog) {
+  const int W = 3 * nb + 1;
+  const int G = gridDim.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int NW = 4;
+  __shared__ double v[32];
+  __shared__ double wv[96];
+  __shared__ double sh[4];
+  volatile int* vprog = prog;
+  for (int64_t s = blockIdx.x; s < k - 1; s += G) {
+    const int prev_n = s > 0 ? chase_ntasks(s - 1, k, nb) : 0;
+    ChaseTask tk;
+    int t = 0;
+    for (; chase_task(s, t, k, nb, &tk); ++t) {
+      if (s > 0) {
+        const int need = min(t + 4, prev_n);
+        if (tid == 0)
+          while (vprog[s - 1] < need) __nanosleep(32);
+        __syncthreads();
+        __threadfence();
+      }
+      const int len = (int)(tk.hi - tk.lo + 1);
+      // reflector from the segment (warp 0)
+      if (warp == 0) {
+        double x = 0.0;
+        if (lane < len) {
+          const int64_t r = tk.right ? tk.idx : tk.lo + lane;
+          const int64_t c = tk.right ? tk.lo + lane : tk.idx;
+          x = __ldcg(Bd + band_off(r, c, nb, W));
+        }
+        const double alpha = __shfl_sync(0xffffffffu, x, 0);
+        double ss = lane > 0 ? x * x : 0.0;
+        ss = warp_sum(ss);
+        double tau = 0.0, scal = 0.0, beta = alpha;
+        if (ss > 0.0) {
+          beta = -copysign(sqrt(alpha * alpha + ss), alpha);
+          tau = (beta - alpha) / beta;
+          scal = 1.0 / (alpha - beta);
+        }
+        v[lane] = lane == 0 ? 1.0 : (lane < len ? x * scal : 0.0);
+        if (lane == 0) { sh[0] = tau; sh[1] = beta; }
+      }
+      __syncthreads();
+      const double tau = sh[0];
+      if (tau != 0.0) {
+        if (tk.right) {
+          // rows r in [alo, ahi]: s_r = sum_c M[r, lo + c] v_c ; M[r, .] -= tau s_r v
+          for (int64_t r = tk.alo + warp; r <= tk.ahi; r += NW) {
+            const int64_t c = tk.lo + lane;
+            const bool ok = lane < len && band_in(r, c, nb);
+            double* p = Bd + band_off(r, c, nb, W);
+            const double mv = ok ? __ldcg(p) : 0.0;
+            const double sr = warp_sum(mv * v[lane]) * tau;
+            if (ok) __stcg(p, mv - sr * v[lane]);
+          }
+        } else {
+          // columns c in [alo, ahi]: w_c = sum_r v_r M[lo + r, c] ; M[., c] -= tau v w_c
+          const int ncols = (int)(tk.ahi - tk.alo + 1);
+          for (int cc = tid; cc < ncols; cc += 128) {
+            const int64_t c = tk.alo + cc;
+            double w = 0.0;
+            for (int r = 0; r < len; ++r)
+              if (band_in(tk.lo + r, c, nb)) w += v[r] * __ldcg(Bd + band_off(tk.lo + r, c, nb, W));
+            wv[cc] = w * tau;
+          }
+          __syncthreads();
+          for (int e = tid; e < len * ncols; e += 128) {
+            const int r = e / ncols, cc = e % ncols;
+            const int64_t c = tk.alo + cc;
+            if (band_in(tk.lo + r, c, nb)) {
+              double* p = Bd + band_off(tk.lo + r, c, nb, W);
+              __stcg(p, __ldcg(p) - v[r] * wv[cc]);
+            }
+          }
+        }
+      }
+      __syncthreads();
+      // exact zeros / beta on the annihilated segment
+      if (warp == 0 && lane < len) {
+        const int64_t r = tk.right ? tk.idx : tk.lo + lane;
+        const int64_t c = tk.right ? tk.lo + lane : tk.idx;
+        __stcg(Bd + band_off(r, c, nb, W), lane == 0 ? sh[1] : 0.0);
+      }
+      __syncthreads();
+      if (tid == 0) {
+        __threadfence();
+        atomicExch(prog + s, t + 1);
+      }
+    }
+    if (tid == 0) {
+      __threadfence();
+      atomicExch(prog + s, t + 1000000);  // sweep finished (>= any need)
+    }
+  }
 }
 
 }  // namespace hb

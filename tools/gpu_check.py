@@ -176,11 +176,18 @@ def _():
 @sec("big")
 def _():
     for (d, dp, kname, n) in [(2, 1, "log_r", 16000), (3, 2, "one_over_r", 16000), (4, 3, "exp_neg_r", 8000),
-                              (1, None, "log_r", 65536), (4, 3, "exp_neg_r", 16000)]:
+                              (1, None, "log_r", 65536), (1, None, "log_r", 65536), (2, 1, "log_r", 65536),
+                              (4, 3, "exp_neg_r", 16000), (4, 3, "exp_neg_r", 32000)]:
         seed = O.problem_seed(0, d, dp, n)
         pair = hb.make_pair(d, dp, n, hb.UNIFORM, seed)
         t0 = time.time()
+        ctx.set_profiling(True)
+        L.hb_stats_reset(ctx._h)
         r = ctx.rank(hb.make_kernel(kname), pair, [1e-12])[0]
+        st = ctx.stats()
+        ctx.set_profiling(False)
+        p("   phases ms: " + " ".join(f"{k}={v:.1f}" for k, v in st["phase_ms"].items()) +
+          f" gemm={st['gemm_ms']:.1f}ms {st['gemm_flops']/max(st['gemm_ms'],1e-9)/1e9:.1f}TF")
         p(f"d={d} dp={dp} {kname} N={n}: rank {r.rank} lo/hi {r.rank_lo}/{r.rank_hi} k={r.k_factored} gap {r.gap:.2e} "
           f"resid {r.resid:.2e} sec={[round(s, 4) for s in r.sec]} wall {time.time()-t0:.2f}s "
           f"Gent/s={n*n/r.sec[3]/1e9:.2f}")
