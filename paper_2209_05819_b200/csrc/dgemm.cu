@@ -59,6 +59,7 @@ struct GemmParams {
 
 template <bool TA, int WARPS_M, int WARPS_N, int WM, int WN>
 struct Cfg {
+  static constexpr int NT = WARPS_M * WARPS_N * 32;  // threads per CTA
   static constexpr int BM = WARPS_M * WM * 8;
   static constexpr int BN = WARPS_N * WN * 8;
   static constexpr int BK = 16;
@@ -70,9 +71,11 @@ struct Cfg {
 };
 
 template <bool TA, int WARPS_M, int WARPS_N, int WM, int WN, bool VEC>
-__global__ void __launch_bounds__(256, 1) dgemm_kernel(GemmParams p) {
+__global__ void __launch_bounds__(Cfg<TA, WARPS_M, WARPS_N, WM, WN>::NT,
+                                  Cfg<TA, WARPS_M, WARPS_N, WM, WN>::NT == 128 ? 2 : 1)
+    dgemm_kernel(GemmParams p) {
   using C_ = Cfg<TA, WARPS_M, WARPS_N, WM, WN>;
-  constexpr int BM = C_::BM, BN = C_::BN, BK = C_::BK, STAGES = C_::STAGES;
+  constexpr int BM = C_::BM, BN = C_::BN, BK = C_::BK, STAGES = C_::STAGES, NT = C_::NT;
   extern __shared__ __align__(16) double smem[];
   double* As = smem;
   double* Bs = smem + STAGES * C_::A_ELEMS;
@@ -86,7 +89,7 @@ __global__ void __launch_bounds__(256, 1) dgemm_kernel(GemmParams p) {
   const int nk = kend > kbeg ? (int)((kend - kbeg + BK - 1) / BK) : 0;
   if (p.beta != 0.0 && !p.partial) {
     // warm L2 with this CTA's C tile while the main loop runs (128-byte lines)
-    for (int v = tid; v < BN * (BM / 16); v += 256) {
+    for (int v = tid; v < BN * (BM / 16); v += NT) {
       const int64_t m = m0 + (v % (BM / 16)) * 16, n = n0 + v / (BM / 16);
       if (m < p.M && n < p.N)
         asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p.C + m + n * p.ldc));
@@ -99,7 +102,7 @@ __global__ void __launch_bounds__(256, 1) dgemm_kernel(GemmParams p) {
     double* bs = Bs + stage * C_::B_ELEMS;
     if (!TA) {
       constexpr int VPC = BM / 2;
-      for (int v = tid; v < BK * VPC; v += 256) {
+      for (int v = tid; v < BK * VPC; v += NT) {
         const int kk = v / VPC, mm = (v % VPC) * 2;
         const int64_t gm = m0 + mm, gk = k0 + kk;
         const double* src = p.A + gm + gk * p.lda;
@@ -116,7 +119,7 @@ __global__ void __launch_bounds__(256, 1) dgemm_kernel(GemmParams p) {
       }
     } else {
       constexpr int VPR = BK / 2;
-      for (int v = tid; v < BM * VPR; v += 256) {
+      for (int v = tid; v < BM * VPR; v += NT) {
         const int mm = v / VPR, kk = (v % VPR) * 2;
         const int64_t gm = m0 + mm, gk = k0 + kk;
         const double* src = p.A + gk + gm * p.lda;
@@ -134,7 +137,7 @@ __global__ void __launch_bounds__(256, 1) dgemm_kernel(GemmParams p) {
     }
     {
       constexpr int VPR = BK / 2;
-      for (int v = tid; v < BN * VPR; v += 256) {
+      for (int v = tid; v < BN * VPR; v += NT) {
         const int nn = v / VPR, kk = (v % VPR) * 2;
         const int64_t gn = n0 + nn, gk = k0 + kk;
         const double* src = p.B + gk + gn * p.ldb;
@@ -234,12 +237,12 @@ __global__ void __launch_bounds__(256, 1) dgemm_kernel(GemmParams p) {
         }
     __syncthreads();
     constexpr int VPC = BM / 2;                 // 2-double vectors per column
-    constexpr int PER = VPC * HALF / 256;       // vectors per thread
+    constexpr int PER = VPC * HALF / NT;        // vectors per thread
     double2 cv[PER];
     if (p.beta != 0.0) {
 #pragma unroll
       for (int t = 0; t < PER; ++t) {
-        const int v = tid + t * 256;
+        const int v = tid + t * NT;
         const int ml = (v % VPC) * 2, nl = v / VPC;
         const int64_t m = m0 + ml, n = n0 + half * HALF + nl;
         cv[t] = make_double2(0.0, 0.0);
@@ -255,7 +258,7 @@ __global__ void __launch_bounds__(256, 1) dgemm_kernel(GemmParams p) {
     }
 #pragma unroll
     for (int t = 0; t < PER; ++t) {
-      const int v = tid + t * 256;
+      const int v = tid + t * NT;
       const int ml = (v % VPC) * 2, nl = v / VPC;
       const int64_t m = m0 + ml, n = n0 + half * HALF + nl;
       if (n >= p.N || m >= p.M) continue;
@@ -313,24 +316,28 @@ static void run_cfg(const GemmParams& p, int slices, bool vec, cudaStream_t st) 
   if (vec) {
     auto k = dgemm_kernel<TA, WARPS_M, WARPS_N, WM, WN, true>;
     HB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C_::SMEM));
-    k<<<grid, 256, C_::SMEM, st>>>(p);
+    k<<<grid, C_::NT, C_::SMEM, st>>>(p);
   } else {
     auto k = dgemm_kernel<TA, WARPS_M, WARPS_N, WM, WN, false>;
     HB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C_::SMEM));
-    k<<<grid, 256, C_::SMEM, st>>>(p);
+    k<<<grid, C_::NT, C_::SMEM, st>>>(p);
   }
   HB_LAUNCH_CHECK();
 }
 
 static constexpr int kReduceBlocks = 592;  // 4 x 148 SMs
 
-static int64_t tiles_of(int64_t M, int64_t N) {
+static int64_t tiles_of(int64_t M, int64_t N, int64_t K) {
+  const char* e = getenv("HB_GEMM_CFG");
+  const int cfg = e ? atoi(e) : 0;
   const int bm = M <= 64 ? 64 : 128;
-  return ceil_div(M, bm) * ceil_div(N, 128);
+  const int bn = (M > 64 && cfg != 2) ? 64 : 128;
+  (void)K;
+  return ceil_div(M, bm) * ceil_div(N, bn);
 }
 
 static int choose_slices(int64_t M, int64_t N, int64_t K, int num_sms, int64_t ws_elems) {
-  const int64_t tiles = tiles_of(M, N);
+  const int64_t tiles = tiles_of(M, N, K);
   if (tiles >= num_sms || K < 1024) return 1;
   int64_t s = ceil_div(2 * (int64_t)num_sms, tiles);
   s = std::min<int64_t>(s, K / 512);
@@ -339,7 +346,9 @@ static int choose_slices(int64_t M, int64_t N, int64_t K, int num_sms, int64_t w
   return (int)std::max<int64_t>(s, 1);
 }
 
-int64_t gemm_fro_count(int64_t M, int64_t N) { return std::max<int64_t>(tiles_of(M, N), kReduceBlocks); }
+int64_t gemm_fro_count(int64_t M, int64_t N, int64_t K) {
+  return std::max<int64_t>(tiles_of(M, N, K), kReduceBlocks);
+}
 
 void launch_dgemm(const GemmArgs& g, double* ws, int64_t ws_elems, int num_sms, cudaStream_t st) {
   if (g.M <= 0 || g.N <= 0) return;
@@ -362,9 +371,18 @@ void launch_dgemm(const GemmArgs& g, double* ws, int64_t ws_elems, int num_sms, 
     q.partial = ws;
     q.fro = nullptr;
   }
+  static const int cfg_env = [] {
+    const char* e = getenv("HB_GEMM_CFG");
+    return e ? atoi(e) : 0;
+  }();
   if (g.M <= 64) {
     if (g.transA) run_cfg<true, 1, 8, 8, 2>(q, s_eff, vec, st);
     else run_cfg<false, 1, 8, 8, 2>(q, s_eff, vec, st);
+  } else if (cfg_env != 2) {
+    // 128x64 tiles, 4 warps, 2 CTAs per SM: one CTA's epilogue (C read-modify-write) overlaps the
+    // other's DMMA main loop (measured faster than 128x128 on every rank-reveal shape)
+    if (g.transA) run_cfg<true, 2, 2, 8, 4>(q, s_eff, vec, st);
+    else run_cfg<false, 2, 2, 8, 4>(q, s_eff, vec, st);
   } else {
     if (g.transA) run_cfg<true, 2, 4, 8, 4>(q, s_eff, vec, st);
     else run_cfg<false, 2, 4, 8, 4>(q, s_eff, vec, st);
@@ -376,8 +394,8 @@ void launch_dgemm(const GemmArgs& g, double* ws, int64_t ws_elems, int num_sms, 
   } else if (g.fro_partials) {
     // pad the partial array to the fixed count with zeros so the consumer can always sum
     // gemm_fro_count(M, N) entries
-    const int64_t written = tiles_of(g.M, g.N);
-    const int64_t cnt = gemm_fro_count(g.M, g.N);
+    const int64_t written = tiles_of(g.M, g.N, g.K);
+    const int64_t cnt = gemm_fro_count(g.M, g.N, g.K);
     if (cnt > written)
       HB_CUDA(cudaMemsetAsync(g.fro_partials + written, 0, (cnt - written) * sizeof(double), st));
   }

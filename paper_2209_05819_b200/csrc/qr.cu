@@ -51,6 +51,7 @@ __device__ __forceinline__ bool better(double na, int ia, double nb, int ib) {
 }
 
 __global__ void __launch_bounds__(256) sketch_cpqr_kernel(SketchParams p) {
+  extern __shared__ double nrm_s[];  // norms of this CTA's columns (-1 = chosen)
   const int G = gridDim.x, g = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int ell = p.ell;
@@ -61,19 +62,24 @@ __global__ void __launch_bounds__(256) sketch_cpqr_kernel(SketchParams p) {
   __shared__ int wbi[8];
   __shared__ double sh_tau;
   __shared__ int sh_piv, sh_stop;
+  constexpr int RPL = kSketchRows / 32;  // sketch rows per lane
 
   // init: copy Y -> Ys, exact column norms
   double best = -1.0, sum = 0.0;
   int bi = INT_MAX;
   for (int64_t q = c0 + warp; q < c1; q += 8) {
     double s = 0.0;
-    for (int i = lane; i < ell; i += 32) {
-      const double y = p.Y[i + q * p.ldy];
-      p.Ys[i + q * p.ldy] = y;
-      s += y * y;
+#pragma unroll
+    for (int t = 0; t < RPL; ++t) {
+      const int i = lane + 32 * t;
+      if (i < ell) {
+        const double y = p.Y[i + q * p.ldy];
+        p.Ys[i + q * p.ldy] = y;
+        s += y * y;
+      }
     }
     s = warp_sum(s);
-    if (lane == 0) p.nrm[q] = s;
+    if (lane == 0) nrm_s[q - c0] = s;
     if (better(s, (int)q, best, bi)) { best = s; bi = (int)q; }
     sum += s;
   }
@@ -159,27 +165,68 @@ __global__ void __launch_bounds__(256) sketch_cpqr_kernel(SketchParams p) {
     }
     __syncthreads();
     const double tau = sh_tau;
+    double vr[RPL];
+#pragma unroll
+    for (int t = 0; t < RPL; ++t) {
+      const int i = lane + 32 * t;
+      vr[t] = (i >= c && i < ell) ? v[i] : 0.0;
+    }
     best = -1.0; sum = 0.0; bi = INT_MAX;
-    for (int64_t q = c0 + warp; q < c1; q += 8) {
-      if (q == piv) {
-        if (lane == 0) p.nrm[q] = -1.0;
-        continue;
+    // two columns per warp iteration: all their loads are issued before the first reduction
+    for (int64_t qa = c0 + warp; qa < c1; qa += 16) {
+      const int64_t qb = qa + 8;
+      const bool va = qa != piv && nrm_s[qa - c0] >= 0.0;
+      const bool vb = qb < c1 && qb != piv && nrm_s[qb - c0] >= 0.0;
+      double* ca = p.Ys + qa * p.ldy;
+      double* cb = p.Ys + qb * p.ldy;
+      double ya[RPL], yb[RPL];
+#pragma unroll
+      for (int t = 0; t < RPL; ++t) {
+        const int i = lane + 32 * t;
+        const bool act = i >= c && i < ell;
+        ya[t] = (va && act) ? ca[i] : 0.0;
+        yb[t] = (vb && act) ? cb[i] : 0.0;
       }
-      if (p.nrm[q] < 0.0) continue;  // chosen earlier
-      double* col = p.Ys + q * p.ldy;
-      double w = 0.0;
-      for (int i = c + lane; i < ell; i += 32) w += v[i] * col[i];
-      w = warp_sum(w) * tau;
-      double s = 0.0;
-      for (int i = c + lane; i < ell; i += 32) {
-        const double y = col[i] - w * v[i];
-        col[i] = y;
-        if (i > c) s += y * y;
+      double wa = 0.0, wb = 0.0;
+#pragma unroll
+      for (int t = 0; t < RPL; ++t) { wa += vr[t] * ya[t]; wb += vr[t] * yb[t]; }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        wa += __shfl_xor_sync(0xffffffffu, wa, o);
+        wb += __shfl_xor_sync(0xffffffffu, wb, o);
       }
-      s = warp_sum(s);
-      if (lane == 0) p.nrm[q] = s;
-      if (better(s, (int)q, best, bi)) { best = s; bi = (int)q; }
-      sum += s;
+      wa *= tau; wb *= tau;
+      double sa = 0.0, sb = 0.0;
+#pragma unroll
+      for (int t = 0; t < RPL; ++t) {
+        const int i = lane + 32 * t;
+        const bool act = i >= c && i < ell;
+        const double xa = ya[t] - wa * vr[t], xb = yb[t] - wb * vr[t];
+        if (act) {
+          if (va) ca[i] = xa;
+          if (vb) cb[i] = xb;
+          if (i > c) { sa += xa * xa; sb += xb * xb; }
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        sa += __shfl_xor_sync(0xffffffffu, sa, o);
+        sb += __shfl_xor_sync(0xffffffffu, sb, o);
+      }
+      if (va) {
+        if (lane == 0) nrm_s[qa - c0] = sa;
+        if (better(sa, (int)qa, best, bi)) { best = sa; bi = (int)qa; }
+        sum += sa;
+      } else if (qa == piv && lane == 0) {
+        nrm_s[qa - c0] = -1.0;
+      }
+      if (vb) {
+        if (lane == 0) nrm_s[qb - c0] = sb;
+        if (better(sb, (int)qb, best, bi)) { best = sb; bi = (int)qb; }
+        sum += sb;
+      } else if (qb < c1 && qb == piv && lane == 0) {
+        nrm_s[qb - c0] = -1.0;
+      }
     }
     __syncthreads();
     publish((c + 1) & 1);

@@ -35,6 +35,7 @@ struct PanelParams {
   int64_t ldv;
   double* nslot;   // [G]
   double* wslot;   // [G][b]
+  double* scal;    // [2] published alpha (shared-memory panel kernel)
   GridBarrier bar;
 };
 
@@ -67,6 +68,7 @@ __global__ void sketch_cpqr_kernel(SketchParams p);
 __global__ void permute_kernel(double* A, int64_t lda, int64_t m, double* Y, int64_t ldy, int ell,
                                int64_t* perm, int64_t j, const int* swaps, const int* bptr);
 __global__ void panel_qr_kernel(PanelParams p);
+__global__ void panel_qr_smem_kernel(PanelParams p);
 __global__ void build_T_kernel(const double* S, int64_t lds, const double* tau, int b, double* T,
                                int64_t ldt);
 __global__ void sketch_trsm_kernel(const double* Y1, int64_t ldy, int ell, const double* R,

@@ -53,22 +53,13 @@ struct Gemm {
 };
 
 // Householder panel + compact-WY T.  Panel mp x b at P (ld); V (ld ldv) and T (ld b) out.
-void panel_and_T(hb_context* c, double* P, int64_t ld, int64_t mp, int b, double* V, int64_t ldv,
-                 double* tau, double* T) {
-  const int G = clampi(ceil_div(mp, 256), 1, c->num_sms);
-  PanelParams pp{};
-  pp.P = P; pp.ld = ld; pp.mp = mp; pp.b = b;
-  pp.chunk = ceil_div(mp, G);
-  pp.tau = tau; pp.V = V; pp.ldv = ldv;
-  double* slots = ws<double>(c, B_SLOTS, (size_t)c->num_sms * (kBlockMax + 1) * 2 + 64);
-  pp.nslot = slots;
-  pp.wslot = slots + c->num_sms;
-  pp.bar = barrier(c);
-  const size_t smem = (size_t)(pp.chunk + b) * sizeof(double);
-  HB_REQUIRE(smem <= 200 * 1024, HB_ECAP, "panel: too many rows per CTA");
-  coop(panel_qr_kernel, G, smem, c->stream, pp);
-  // S = VᵀV, T from (S, τ)
-  double* S = ws<double>(c, B_S, kBlockMax * kBlockMax);
+void apply_block_reflector(hb_context* c, const double* V, int64_t ldv, const double* T, int b,
+                           double* A2, int64_t ld, int64_t mp, int64_t n2, double* fro_dev);
+
+// T of the compact-WY form for the b explicit reflectors in V (S = VᵀV by DMMA GEMM).
+void build_T(hb_context* c, const double* V, int64_t ldv, int64_t mp, int b, const double* tau,
+             double* T, int bufid) {
+  double* S = ws<double>(c, bufid, kBlockMax * kBlockMax);
   GemmArgs g{};
   g.M = b; g.N = b; g.K = mp; g.alpha = 1.0; g.A = V; g.lda = ldv; g.transA = true;
   g.B = V; g.ldb = ldv; g.beta = 0.0; g.C = S; g.ldc = b;
@@ -79,6 +70,63 @@ void panel_and_T(hb_context* c, double* P, int64_t ld, int64_t mp, int b, double
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm));
   build_T_kernel<<<1, 128, tsm, c->stream>>>(S, b, tau, b, T, b);
   HB_LAUNCH_CHECK();
+}
+
+// Householder QR of the mp x b panel at P (ld): R and V in place, explicit V (ld ldv), τ, and T
+// (ld b) of Q = I − V T Vᵀ.  The shared-memory-resident kernel handles up to ~200 KB of panel
+// rows per CTA; wider panels are factored as column sub-panels joined by a block-reflector
+// GEMM update (left-looking within the panel).
+void panel_and_T(hb_context* c, double* P, int64_t ld, int64_t mp, int b, double* V, int64_t ldv,
+                 double* tau, double* T) {
+  cudaStream_t st = c->stream;
+  double* slots = ws<double>(c, B_SLOTS, (size_t)c->num_sms * (kBlockMax + 1) * 2 + 64);
+  double* scal2 = ws<double>(c, B_PSCAL, 8);
+  const int G = clampi(ceil_div(mp, 64), 1, c->num_sms);
+  const int64_t chunk = ceil_div(mp, G);
+  const int64_t budget = (200 * 1024) / 8;  // doubles of shared memory per CTA
+  int bsub = (int)std::min<int64_t>(b, budget / (chunk + 2) - 1);
+  if (bsub >= 8 && bsub < b) bsub &= ~7;
+  if (bsub < 8 && bsub < b) {
+    // very tall panel: global-memory fallback kernel
+    PanelParams pp{};
+    pp.P = P; pp.ld = ld; pp.mp = mp; pp.b = b;
+    const int Gf = clampi(ceil_div(mp, 256), 1, c->num_sms);
+    pp.chunk = ceil_div(mp, Gf);
+    pp.tau = tau; pp.V = V; pp.ldv = ldv;
+    pp.nslot = slots; pp.wslot = slots + c->num_sms;
+    pp.bar = barrier(c);
+    const size_t smem = (size_t)(pp.chunk + b) * sizeof(double);
+    HB_REQUIRE(smem <= 200 * 1024, HB_ECAP, "panel: too many rows per CTA");
+    coop(panel_qr_kernel, Gf, smem, st, pp);
+    build_T(c, V, ldv, mp, b, tau, T, B_S);
+    return;
+  }
+  double* Tsub = ws<double>(c, B_TSUB, kBlockMax * kBlockMax);
+  for (int c0 = 0; c0 < b; c0 += bsub) {
+    const int bs = std::min(bsub, b - c0);
+    const int64_t mps = mp - c0;
+    if (c0 > 0) HB_CUDA(cudaMemset2DAsync(V + c0 * ldv, ldv * 8, 0, c0 * 8, bs, st));
+    if (mps <= 0) {  // wide LQ panel ran out of rows: no more reflectors
+      HB_CUDA(cudaMemsetAsync(tau + c0, 0, (b - c0) * sizeof(double), st));
+      HB_CUDA(cudaMemset2DAsync(V + c0 * ldv, ldv * 8, 0, mp * 8, b - c0, st));
+      break;
+    }
+    PanelParams pp{};
+    pp.P = P + c0 + c0 * ld; pp.ld = ld; pp.mp = mps; pp.b = bs;
+    const int Gs = clampi(ceil_div(mps, 64), 1, c->num_sms);
+    pp.chunk = ceil_div(mps, Gs);
+    pp.tau = tau + c0; pp.V = V + c0 + c0 * ldv; pp.ldv = ldv;
+    pp.nslot = slots; pp.wslot = slots + c->num_sms; pp.scal = scal2;
+    pp.bar = barrier(c);
+    const size_t smem = ((size_t)bs * (pp.chunk + 1) + bs) * sizeof(double);
+    coop(panel_qr_smem_kernel, Gs, smem, st, pp);
+    if (c0 + bs < b) {
+      build_T(c, V + c0 + c0 * ldv, ldv, mps, bs, tau + c0, Tsub, B_S);
+      apply_block_reflector(c, V + c0 + c0 * ldv, ldv, Tsub, bs, P + c0 + (c0 + bs) * ld, ld, mps,
+                            b - c0 - bs, nullptr);
+    }
+  }
+  build_T(c, V, ldv, mp, b, tau, T, B_S);
 }
 
 // A2 (mp x n2, ld) ← (I − V Tᵀ Vᵀ) A2; if fro != nullptr the exact sum of squares of rows >= b of
@@ -103,7 +151,7 @@ void apply_block_reflector(hb_context* c, const double* V, int64_t ldv, const do
   double* parts = nullptr;
   int64_t cnt = 0;
   if (fro_dev) {
-    cnt = gemm_fro_count(mp, n2);
+    cnt = gemm_fro_count(mp, n2, b);
     parts = ws<double>(c, B_FRO, (size_t)cnt);
     g3.fro_partials = parts;
     g3.fro_row0 = b;
@@ -219,7 +267,7 @@ void rank_matrix_inplace(hb_context* c, double* A, int64_t m, int64_t n, int64_t
   int* beff = ws<int>(c, B_BEFF, 4);
   int64_t* perm = ws<int64_t>(c, B_PERM, (size_t)n);
   double* scal = ws<double>(c, B_FROSUM, 8);  // [0] fro², [1] σ̂₁
-  double* sk_slots = ws<double>(c, B_SCAL, (size_t)c->num_sms * 6 + 16);
+  double* sk_slots = ws<double>(c, B_SCAL, (size_t)c->num_sms * 12 + 16);  // [2][G <= 2 SMs][3]
   iota_kernel<<<(unsigned)ceil_div(std::max<int64_t>(n, 1), 256), 256, 0, c->stream>>>(perm, n);
   HB_LAUNCH_CHECK();
 
@@ -234,147 +282,161 @@ void rank_matrix_inplace(hb_context* c, double* A, int64_t m, int64_t n, int64_t
   double sigma1_est = 0.0, delta = 0.0, fro_at_sketch = INFINITY;
   bool first = true;
   int zero_retries = 0;
-  while (j < kmax) {
-    const int b_req = (int)std::min<int64_t>({(int64_t)b, kmax - j, (int64_t)kBlockMax});
-    const int64_t n_tr = n - j, mp = m - j;
-    SketchParams sp{};
-    sp.Y = Y + j * ell; sp.Ys = Ys; sp.nrm = nrm; sp.ell = ell; sp.ldy = ell; sp.n_tr = n_tr;
-    sp.b_req = b_req; sp.b_min = std::min(8, b_req);
-    const double stop_res = 0.5 * c->eta * tol_min * sigma1_est;
-    sp.stop_fro2 = sigma1_est > 0.0 ? stop_res * stop_res : -1.0;
-    sp.slots = sk_slots; sp.piv = piv; sp.swaps = swaps; sp.rdiag = rdiag; sp.out_est = est;
-    sp.out_b = beff; sp.bar = barrier(c);
-    {
-      Phase ph(c, HB_PH_PIVOT);
-      coop(sketch_cpqr_kernel, clampi(ceil_div(n_tr, 128), 1, c->num_sms), 0, st, sp);
-    }
-    int bh = 0;
-    sync_to_host(c, beff, &bh, sizeof(int));
-    if (bh == 0) {
-      // the sketch of the trailing matrix vanished: re-sketch once, else the trailing block is 0
-      if (zero_retries++ < 1) {
-        Phase ph(c, HB_PH_SKETCH);
-        sketch_seed = splitmix64(sketch_seed);
-        double* Om = ws<double>(c, B_OMEGA, (size_t)ell * std::max<int64_t>(mp, 1));
-        launch_gaussian(Om, ell, mp, ell, sketch_seed, st);
+  // Factor until ||A22||_F <= eta·tol·σ̂₁, certify, and only if some bracket stays open
+  // (a σ(R_k) inside the window (sqrt(thr² − δ²), thr]) resume the factorisation with a 5x
+  // smaller eta and certify again.  The bracket is rigorous for any δ; eta trades columns
+  // (work) against the chance of a re-certification.
+  double eta_cur = c->eta;
+  SigmaAnswer ans[HB_MAX_TOLS];
+  int64_t k = 0;
+  int rounds = 0;
+  for (;; ++rounds) {
+    while (j < kmax) {
+      const int b_req = (int)std::min<int64_t>({(int64_t)b, kmax - j, (int64_t)kBlockMax});
+      const int64_t n_tr = n - j, mp = m - j;
+      SketchParams sp{};
+      sp.Y = Y + j * ell; sp.Ys = Ys; sp.nrm = nrm; sp.ell = ell; sp.ldy = ell; sp.n_tr = n_tr;
+      sp.b_req = b_req; sp.b_min = std::min(8, b_req);
+      const double stop_res = 0.5 * eta_cur * tol_min * sigma1_est;
+      sp.stop_fro2 = sigma1_est > 0.0 ? stop_res * stop_res : -1.0;
+      sp.slots = sk_slots; sp.piv = piv; sp.swaps = swaps; sp.rdiag = rdiag; sp.out_est = est;
+      sp.out_b = beff; sp.bar = barrier(c);
+      {
+        Phase ph(c, HB_PH_PIVOT);
+        const int Gs = clampi(ceil_div(n_tr, 64), 1, 2 * c->num_sms);
+        coop(sketch_cpqr_kernel, Gs, (size_t)ceil_div(n_tr, Gs) * sizeof(double), st, sp);
+      }
+      int bh = 0;
+      sync_to_host(c, beff, &bh, sizeof(int));
+      if (bh == 0) {
+        // the sketch of the trailing matrix vanished: re-sketch once, else the trailing block is 0
+        if (zero_retries++ < 1) {
+          Phase ph(c, HB_PH_SKETCH);
+          sketch_seed = splitmix64(sketch_seed);
+          double* Om = ws<double>(c, B_OMEGA, (size_t)ell * std::max<int64_t>(mp, 1));
+          launch_gaussian(Om, ell, mp, ell, sketch_seed, st);
+          GemmArgs g{};
+          g.M = ell; g.N = n_tr; g.K = mp; g.alpha = 1.0; g.A = Om; g.lda = ell;
+          g.B = A + j + j * lda; g.ldb = lda; g.beta = 0.0; g.C = Y + j * ell; g.ldc = ell;
+          Gemm{c}(g);
+          continue;
+        }
+        break;
+      }
+      zero_retries = 0;
+      {
+        Phase ph(c, HB_PH_PIVOT);
+        permute_kernel<<<(unsigned)ceil_div(m + ell + 1, 256), 256, 0, st>>>(A, lda, m, Y, ell, ell,
+                                                                               perm, j, swaps, beff);
+        HB_LAUNCH_CHECK();
+      }
+      double* P = A + j + j * lda;
+      {
+        Phase ph(c, HB_PH_PANEL);
+        panel_and_T(c, P, lda, mp, bh, V, ldv, tau, T);
+      }
+      const int64_t n2 = n - j - bh;
+      Phase ph_up(c, HB_PH_UPDATE);
+      if (n2 > 0 && mp > bh) {
+        apply_block_reflector(c, V, ldv, T, bh, A + j + (j + bh) * lda, lda, mp, n2, scal);
+      } else {
+        if (n2 > 0) apply_block_reflector(c, V, ldv, T, bh, A + j + (j + bh) * lda, lda, mp, n2, nullptr);
+        HB_CUDA(cudaMemsetAsync(scal, 0, sizeof(double), st));
+      }
+      ph_up.close();
+      if (first) {
+        Phase ph(c, HB_PH_SIGMA1);
+        PowerParams pw{};
+        pw.R = A; pw.ld = lda; pw.b = bh; pw.n = n; pw.iters = 40;
+        pw.slots = ws<double>(c, B_SIG1, (size_t)2 * c->num_sms * (kBlockMax + 1));
+        pw.out = scal + 1; pw.bar = barrier(c);
+        coop(power_sigma1_kernel, clampi(ceil_div(n, 256), 1, c->num_sms), 0, st, pw);
+      }
+      if (n2 > 0) {
+        Phase ph(c, HB_PH_DOWNDATE);
+        const size_t rsm = (size_t)bh * bh * sizeof(double);
+        if (rsm > 48 * 1024)
+          HB_CUDA(cudaFuncSetAttribute((const void*)sketch_trsm_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm));
+        sketch_trsm_kernel<<<1, ell, rsm, st>>>(Y + j * ell, ell, ell, P, lda, bh, Z, ell);
+        HB_LAUNCH_CHECK();
         GemmArgs g{};
-        g.M = ell; g.N = n_tr; g.K = mp; g.alpha = 1.0; g.A = Om; g.lda = ell;
+        g.M = ell; g.N = n2; g.K = bh; g.alpha = -1.0; g.A = Z; g.lda = ell;
+        g.B = A + j + (j + bh) * lda; g.ldb = lda; g.beta = 1.0; g.C = Y + (j + bh) * ell; g.ldc = ell;
+        Gemm{c}(g);
+      }
+      j += bh;
+      double hs[2];
+      sync_to_host(c, scal, hs, sizeof(hs));
+      delta = std::sqrt(std::max(hs[0], 0.0));
+      if (first) {
+        sigma1_est = hs[1];
+        first = false;
+      }
+      if (j >= kmax) break;
+      if (delta <= eta_cur * tol_min * sigma1_est) break;
+      if (!(fro_at_sketch < INFINITY)) fro_at_sketch = delta;
+      if (delta < 1e-8 * fro_at_sketch) {
+        Phase ph(c, HB_PH_SKETCH);
+        // the downdated sketch has lost ~8 digits to cancellation: draw a fresh one
+        sketch_seed = splitmix64(sketch_seed);
+        const int64_t mr = m - j;
+        double* Om = ws<double>(c, B_OMEGA, (size_t)ell * std::max<int64_t>(mr, 1));
+        launch_gaussian(Om, ell, mr, ell, sketch_seed, st);
+        GemmArgs g{};
+        g.M = ell; g.N = n - j; g.K = mr; g.alpha = 1.0; g.A = Om; g.lda = ell;
         g.B = A + j + j * lda; g.ldb = lda; g.beta = 0.0; g.C = Y + j * ell; g.ldc = ell;
         Gemm{c}(g);
-        continue;
+        fro_at_sketch = delta;
       }
-      break;
+      b = std::min(2 * b, c->block_max);
     }
-    zero_retries = 0;
-    {
-      Phase ph(c, HB_PH_PIVOT);
-      permute_kernel<<<(unsigned)ceil_div(m + ell + 1, 256), 256, 0, st>>>(A, lda, m, Y, ell, ell,
-                                                                             perm, j, swaps, beff);
-      HB_LAUNCH_CHECK();
-    }
-    double* P = A + j + j * lda;
-    {
-      Phase ph(c, HB_PH_PANEL);
-      panel_and_T(c, P, lda, mp, bh, V, ldv, tau, T);
-    }
-    const int64_t n2 = n - j - bh;
-    Phase ph_up(c, HB_PH_UPDATE);
-    if (n2 > 0 && mp > bh) {
-      apply_block_reflector(c, V, ldv, T, bh, A + j + (j + bh) * lda, lda, mp, n2, scal);
-    } else {
-      if (n2 > 0) apply_block_reflector(c, V, ldv, T, bh, A + j + (j + bh) * lda, lda, mp, n2, nullptr);
-      HB_CUDA(cudaMemsetAsync(scal, 0, sizeof(double), st));
-    }
-    ph_up.close();
-    if (first) {
-      Phase ph(c, HB_PH_SIGMA1);
-      PowerParams pw{};
-      pw.R = A; pw.ld = lda; pw.b = bh; pw.n = n; pw.iters = 40;
-      pw.slots = ws<double>(c, B_SIG1, (size_t)2 * c->num_sms * (kBlockMax + 1));
-      pw.out = scal + 1; pw.bar = barrier(c);
-      coop(power_sigma1_kernel, clampi(ceil_div(n, 256), 1, c->num_sms), 0, st, pw);
-    }
-    if (n2 > 0) {
-      Phase ph(c, HB_PH_DOWNDATE);
-      const size_t rsm = (size_t)bh * bh * sizeof(double);
-      if (rsm > 48 * 1024)
-        HB_CUDA(cudaFuncSetAttribute((const void*)sketch_trsm_kernel,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm));
-      sketch_trsm_kernel<<<1, ell, rsm, st>>>(Y + j * ell, ell, ell, P, lda, bh, Z, ell);
-      HB_LAUNCH_CHECK();
-      GemmArgs g{};
-      g.M = ell; g.N = n2; g.K = bh; g.alpha = -1.0; g.A = Z; g.lda = ell;
-      g.B = A + j + (j + bh) * lda; g.ldb = lda; g.beta = 1.0; g.C = Y + (j + bh) * ell; g.ldc = ell;
-      Gemm{c}(g);
-    }
-    j += bh;
-    double hs[2];
-    sync_to_host(c, scal, hs, sizeof(hs));
-    delta = std::sqrt(std::max(hs[0], 0.0));
-    if (first) {
-      sigma1_est = hs[1];
-      first = false;
-    }
-    if (j >= kmax) break;
-    if (delta <= c->eta * tol_min * sigma1_est) break;
-    if (!(fro_at_sketch < INFINITY)) fro_at_sketch = delta;
-    if (delta < 1e-8 * fro_at_sketch) {
-      Phase ph(c, HB_PH_SKETCH);
-      // the downdated sketch has lost ~8 digits to cancellation: draw a fresh one
-      sketch_seed = splitmix64(sketch_seed);
-      const int64_t mr = m - j;
-      double* Om = ws<double>(c, B_OMEGA, (size_t)ell * std::max<int64_t>(mr, 1));
-      launch_gaussian(Om, ell, mr, ell, sketch_seed, st);
-      GemmArgs g{};
-      g.M = ell; g.N = n - j; g.K = mr; g.alpha = 1.0; g.A = Om; g.lda = ell;
-      g.B = A + j + j * lda; g.ldb = lda; g.beta = 0.0; g.C = Y + j * ell; g.ldc = ell;
-      Gemm{c}(g);
-      fro_at_sketch = delta;
-    }
-    b = std::min(2 * b, c->block_max);
-  }
-  if (j >= kmax) delta = 0.0;
-  const int64_t k = j;
-  HB_CUDA(cudaEventRecord(c->ev[2], st));
+    if (j >= kmax) delta = 0.0;
+    k = j;
+    HB_CUDA(cudaEventRecord(c->ev[2], st));
 
-  // ---- certification: σ(R_k) ------------------------------------------------------------
-  SigmaQuery hq[HB_MAX_TOLS];
-  for (int t = 0; t < ntol; ++t) hq[t] = SigmaQuery{tols[t], delta};
-  SigmaAnswer ans[HB_MAX_TOLS];
-  std::memset(ans, 0, sizeof(ans));
-  if (k > 0) {
-    const int64_t ldb = round_up(n, 8);
-    double* Bc = ws<double>(c, B_CERT_B, (size_t)ldb * k);
-    dim3 tb(32, 8), tg((unsigned)ceil_div(n, 32), (unsigned)ceil_div(k, 32));
-    Phase ph_qr(c, HB_PH_CERT_QR);
-    transpose_upper_kernel<<<tg, tb, 0, st>>>(A, lda, k, n, Bc, ldb);
-    HB_LAUNCH_CHECK();
-    const int bq_max = kBlockMax;
-    for (int64_t jj = 0; jj < k; jj += bq_max) {
-      const int bq = (int)std::min<int64_t>(bq_max, k - jj);
-      double* P = Bc + jj + jj * ldb;
-      panel_and_T(c, P, ldb, n - jj, bq, V, ldv, tau, T);
-      if (jj + bq < k)
-        apply_block_reflector(c, V, ldv, T, bq, Bc + jj + (jj + bq) * ldb, ldb, n - jj,
-                              k - jj - bq, nullptr);
+    // ---- certification: σ(R_k) ------------------------------------------------------------
+    SigmaQuery hq[HB_MAX_TOLS];
+    for (int t = 0; t < ntol; ++t) hq[t] = SigmaQuery{tols[t], delta};
+    std::memset(ans, 0, sizeof(ans));
+    if (k > 0) {
+      const int64_t ldb = round_up(n, 8);
+      double* Bc = ws<double>(c, B_CERT_B, (size_t)ldb * k);
+      dim3 tb(32, 8), tg((unsigned)ceil_div(n, 32), (unsigned)ceil_div(k, 32));
+      Phase ph_qr(c, HB_PH_CERT_QR);
+      transpose_upper_kernel<<<tg, tb, 0, st>>>(A, lda, k, n, Bc, ldb);
+      HB_LAUNCH_CHECK();
+      const int bq_max = kBlockMax;
+      for (int64_t jj = 0; jj < k; jj += bq_max) {
+        const int bq = (int)std::min<int64_t>(bq_max, k - jj);
+        double* P = Bc + jj + jj * ldb;
+        panel_and_T(c, P, ldb, n - jj, bq, V, ldv, tau, T);
+        if (jj + bq < k)
+          apply_block_reflector(c, V, ldv, T, bq, Bc + jj + (jj + bq) * ldb, ldb, n - jj,
+                                k - jj - bq, nullptr);
+      }
+      const int64_t ldm = round_up(k, 8);
+      double* Mk = ws<double>(c, B_CERT_M, (size_t)ldm * k);
+      copy_upper_kernel<<<(unsigned)ceil_div(k * k, 256), 256, 0, st>>>(Bc, ldb, k, Mk, ldm);
+      HB_LAUNCH_CHECK();
+      ph_qr.close();
+      Phase ph_bd(c, HB_PH_BIDIAG);
+      double* d = ws<double>(c, B_D, (size_t)k + 1);
+      double* e = ws<double>(c, B_E, (size_t)k + 1);
+      two_stage_bidiag(c, Mk, ldm, k, d, e, V, ldv, tau, T);
+      ph_bd.close();
+      Phase ph_bs(c, HB_PH_BISECT);
+      SigmaQuery* dq = ws<SigmaQuery>(c, B_QUERY, HB_MAX_TOLS);
+      SigmaAnswer* da = ws<SigmaAnswer>(c, B_ANSWER, HB_MAX_TOLS);
+      HB_CUDA(cudaMemcpyAsync(dq, hq, sizeof(SigmaQuery) * ntol, cudaMemcpyHostToDevice, st));
+      sigma_queries_kernel<<<1, 32 * HB_MAX_TOLS, 0, st>>>(d, e, k, dq, ntol, da);
+      HB_LAUNCH_CHECK();
+      sync_to_host(c, da, ans, sizeof(SigmaAnswer) * ntol);
     }
-    const int64_t ldm = round_up(k, 8);
-    double* Mk = ws<double>(c, B_CERT_M, (size_t)ldm * k);
-    copy_upper_kernel<<<(unsigned)ceil_div(k * k, 256), 256, 0, st>>>(Bc, ldb, k, Mk, ldm);
-    HB_LAUNCH_CHECK();
-    ph_qr.close();
-    Phase ph_bd(c, HB_PH_BIDIAG);
-    double* d = ws<double>(c, B_D, (size_t)k + 1);
-    double* e = ws<double>(c, B_E, (size_t)k + 1);
-    two_stage_bidiag(c, Mk, ldm, k, d, e, V, ldv, tau, T);
-    ph_bd.close();
-    Phase ph_bs(c, HB_PH_BISECT);
-    SigmaQuery* dq = ws<SigmaQuery>(c, B_QUERY, HB_MAX_TOLS);
-    SigmaAnswer* da = ws<SigmaAnswer>(c, B_ANSWER, HB_MAX_TOLS);
-    HB_CUDA(cudaMemcpyAsync(dq, hq, sizeof(SigmaQuery) * ntol, cudaMemcpyHostToDevice, st));
-    sigma_queries_kernel<<<1, 32 * HB_MAX_TOLS, 0, st>>>(d, e, k, dq, ntol, da);
-    HB_LAUNCH_CHECK();
-    sync_to_host(c, da, ans, sizeof(SigmaAnswer) * ntol);
+    bool open = false;
+    for (int t = 0; t < ntol; ++t) open |= ans[t].rank_lo != ans[t].rank_hi;
+    if (!open || j >= kmax || rounds >= 3) break;
+    eta_cur *= 0.2;
   }
   HB_CUDA(cudaEventRecord(c->ev[3], st));
   HB_CUDA(cudaEventSynchronize(c->ev[3]));

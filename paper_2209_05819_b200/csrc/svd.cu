@@ -406,32 +406,51 @@ __global__ void __launch_bounds__(128) bulge_chase_kernel(double* __restrict__ B
       const double tau = sh[0];
       if (tau != 0.0) {
         if (tk.right) {
-          // rows r in [alo, ahi]: s_r = sum_c M[r, lo + c] v_c ; M[r, .] -= tau s_r v
-          for (int64_t r = tk.alo + warp; r <= tk.ahi; r += NW) {
-            const int64_t c = tk.lo + lane;
-            const bool ok = lane < len && band_in(r, c, nb);
-            double* p = Bd + band_off(r, c, nb, W);
-            const double mv = ok ? __ldcg(p) : 0.0;
-            const double sr = warp_sum(mv * v[lane]) * tau;
-            if (ok) __stcg(p, mv - sr * v[lane]);
+          // rows r in [alo, ahi]: s_r = sum_c M[r, lo + c] v_c ; M[r, .] -= tau s_r v.
+          // A warp owns up to 16 rows; all their loads are issued before the reductions.
+          constexpr int RMAX = 16;
+          const int64_t c = tk.lo + lane;
+          const double vl = v[lane];
+          double mv[RMAX];
+#pragma unroll
+          for (int j = 0; j < RMAX; ++j) {
+            const int64_t r = tk.alo + warp + (int64_t)j * NW;
+            const bool ok = r <= tk.ahi && lane < len && band_in(r, c, nb);
+            mv[j] = ok ? __ldcg(Bd + band_off(r, c, nb, W)) : 0.0;
+          }
+          double sr[RMAX];
+#pragma unroll
+          for (int j = 0; j < RMAX; ++j) sr[j] = mv[j] * vl;
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+            for (int j = 0; j < RMAX; ++j) sr[j] += __shfl_xor_sync(0xffffffffu, sr[j], o);
+#pragma unroll
+          for (int j = 0; j < RMAX; ++j) {
+            const int64_t r = tk.alo + warp + (int64_t)j * NW;
+            const bool ok = r <= tk.ahi && lane < len && band_in(r, c, nb);
+            if (ok) __stcg(Bd + band_off(r, c, nb, W), mv[j] - tau * sr[j] * vl);
           }
         } else {
-          // columns c in [alo, ahi]: w_c = sum_r v_r M[lo + r, c] ; M[., c] -= tau v w_c
+          // columns c in [alo, ahi] (one per thread): w_c = sum_r v_r M[lo + r, c];
+          // M[., c] -= tau v w_c.  The column segment is held in registers.
           const int ncols = (int)(tk.ahi - tk.alo + 1);
           for (int cc = tid; cc < ncols; cc += 128) {
             const int64_t c = tk.alo + cc;
+            double x[32];
+#pragma unroll
+            for (int r = 0; r < 32; ++r) {
+              const bool ok = r < len && band_in(tk.lo + r, c, nb);
+              x[r] = ok ? __ldcg(Bd + band_off(tk.lo + r, c, nb, W)) : 0.0;
+            }
             double w = 0.0;
-            for (int r = 0; r < len; ++r)
-              if (band_in(tk.lo + r, c, nb)) w += v[r] * __ldcg(Bd + band_off(tk.lo + r, c, nb, W));
-            wv[cc] = w * tau;
-          }
-          __syncthreads();
-          for (int e = tid; e < len * ncols; e += 128) {
-            const int r = e / ncols, cc = e % ncols;
-            const int64_t c = tk.alo + cc;
-            if (band_in(tk.lo + r, c, nb)) {
-              double* p = Bd + band_off(tk.lo + r, c, nb, W);
-              __stcg(p, __ldcg(p) - v[r] * wv[cc]);
+#pragma unroll
+            for (int r = 0; r < 32; ++r) w += v[r] * x[r];
+            w *= tau;
+#pragma unroll
+            for (int r = 0; r < 32; ++r) {
+              const bool ok = r < len && band_in(tk.lo + r, c, nb);
+              if (ok) __stcg(Bd + band_off(tk.lo + r, c, nb, W), x[r] - v[r] * w);
             }
           }
         }

@@ -1,0 +1,308 @@
+// hb200.hpp — C++ host mirror of the reference interface for the rank-reveal path, over the C ABI
+// (include/hb.h).  Same names, argument meaning and error behaviour as the reference headers, so
+// a caller of hodlr::KernelSpec / HyperCube / InteractionClass / (SPEC) pair_geometry,
+// epsilon_rank, rank_table can switch to hb200:: with the device doing the work.
+//
+//   hb200::KernelId / KernelSpec / kernel_from_string / kernel_name / eval_radial
+//        <- hodlr::KernelId, KernelSpec, kernel_from_string, kernel_name, eval_radial
+//           (/root/reference/proj/include/hodlr/kernel.hpp:19-157)
+//   hb200::HyperCube, InteractionClass   <- hodlr::HyperCube, InteractionClass (geometry.hpp:15-104)
+//   hb200::pair_geometry, epsilon_rank, rank_table, RankRecord, write_csv
+//        <- SPEC rankbench module (CSV schema SPEC.md:613)
+// Exceptions follow the reference: std::invalid_argument (HB_EINVAL), std::length_error
+// (HB_ECAP), std::domain_error (HB_EDOMAIN), std::runtime_error (HB_ESINGULAR and device
+// errors).  KernelId::Custom (a std::function) cannot run on the device: EUNSUPPORTED ->
+// std::invalid_argument with an explanatory message.
+#pragma once
+
+#include <cstdint>
+#include <optional>
+#include <ostream>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "hb.h"
+
+namespace hb200 {
+
+inline void check(hb_status s, const char* where, const hb_context* ctx = nullptr) {
+  if (s == HB_OK) return;
+  std::string msg = std::string(where) + ": " + hb_status_string(s);
+  const char* detail = hb_last_error(ctx);
+  if (detail && *detail) msg += std::string(" (") + detail + ")";
+  switch (s) {
+    case HB_EINVAL:
+    case HB_EUNSUPPORTED: throw std::invalid_argument(msg);
+    case HB_ECAP: throw std::length_error(msg);
+    case HB_EDOMAIN: throw std::domain_error(msg);
+    default: throw std::runtime_error(msg);
+  }
+}
+
+enum class KernelId {
+  InverseR, LogR, Helmholtz3DReal, Helmholtz3DImag, HankelH12Real, HankelH12Imag, R, SinR,
+  InvSqrt1PlusR, ExpNegR, ExpNegR2, Custom,
+};
+
+struct KernelSpec {
+  KernelId id = KernelId::Custom;
+  std::optional<double> diagonal_value;
+
+  static KernelSpec catalog(KernelId id) {  // kernel.hpp:40-67
+    if (id == KernelId::Custom)
+      throw std::invalid_argument("KernelSpec::catalog: Custom has no catalog entry");
+    KernelSpec s;
+    s.id = id;
+    switch (id) {
+      case KernelId::Helmholtz3DImag:
+      case KernelId::InvSqrt1PlusR:
+      case KernelId::ExpNegR:
+      case KernelId::ExpNegR2: s.diagonal_value = 1.0; break;
+      default: s.diagonal_value = 0.0; break;
+    }
+    return s;
+  }
+  bool singular_at_origin() const {
+    return id == KernelId::InverseR || id == KernelId::LogR || id == KernelId::Helmholtz3DReal ||
+           id == KernelId::HankelH12Imag || (id == KernelId::Custom && !diagonal_value);
+  }
+  hb_kernel to_c() const {
+    hb_kernel k{};
+    k.id = static_cast<int32_t>(id);
+    k.has_diag = diagonal_value.has_value();
+    k.diag = diagonal_value.value_or(0.0);
+    return k;
+  }
+};
+
+inline const std::vector<std::pair<std::string, KernelId>>& kernel_names() {
+  static const std::vector<std::pair<std::string, KernelId>> t = {
+      {"one_over_r", KernelId::InverseR}, {"log_r", KernelId::LogR},
+      {"helmholtz3d_re", KernelId::Helmholtz3DReal}, {"helmholtz3d_im", KernelId::Helmholtz3DImag},
+      {"hankel_h12_re", KernelId::HankelH12Real}, {"hankel_h12_im", KernelId::HankelH12Imag},
+      {"r", KernelId::R}, {"sin_r", KernelId::SinR}, {"inv_sqrt_1_plus_r", KernelId::InvSqrt1PlusR},
+      {"exp_neg_r", KernelId::ExpNegR}, {"exp_neg_r2", KernelId::ExpNegR2}};
+  return t;
+}
+
+inline KernelSpec kernel_from_string(const std::string& name) {  // kernel.hpp:112-129
+  for (const auto& [key, id] : kernel_names())
+    if (name == key) return KernelSpec::catalog(id);
+  throw std::invalid_argument("unknown kernel id: " + name);
+}
+
+inline std::string kernel_name(const KernelSpec& spec) {
+  for (const auto& [key, id] : kernel_names())
+    if (spec.id == id) return key;
+  return "custom";
+}
+
+inline double eval_radial(const KernelSpec& spec, double r) {  // kernel.hpp:149-157
+  const hb_kernel k = spec.to_c();
+  double out = 0.0;
+  check(hb_eval_radial_host(&k, r, &out), "eval_radial");
+  return out;
+}
+
+struct HyperCube {  // geometry.hpp:15-64
+  std::vector<double> lower;
+  double side = 1.0;
+  HyperCube() = default;
+  HyperCube(std::vector<double> lower_corner, double side_length)
+      : lower(std::move(lower_corner)), side(side_length) {
+    if (!(side > 0.0)) throw std::invalid_argument("HyperCube: side must be positive");
+    if (lower.empty() || lower.size() > 8) throw std::invalid_argument("HyperCube: 1 <= d <= 8");
+  }
+  int dim() const { return static_cast<int>(lower.size()); }
+  hb_cube to_c() const {
+    hb_cube c{};
+    c.d = dim();
+    for (int k = 0; k < dim(); ++k) c.lower[k] = lower[k];
+    c.side = side;
+    return c;
+  }
+};
+
+struct InteractionClass {  // geometry.hpp:77-104
+  enum class Kind { SelfBlock, SharedSurface, FarField };
+  Kind kind = Kind::SelfBlock;
+  int surface_dim = -1;
+  static InteractionClass self_block() { return {Kind::SelfBlock, -1}; }
+  static InteractionClass shared_surface(int d_prime) { return {Kind::SharedSurface, d_prime}; }
+  static InteractionClass far_field() { return {Kind::FarField, -1}; }
+  bool is_far() const { return kind == Kind::FarField; }
+  bool is_vertex() const { return kind == Kind::SharedSurface && surface_dim == 0; }
+  std::string name() const {
+    switch (kind) {
+      case Kind::SelfBlock: return "self";
+      case Kind::FarField: return "far";
+      default: return "surface:" + std::to_string(surface_dim);
+    }
+  }
+  static InteractionClass parse(const std::string& s) {
+    if (s == "far") return far_field();
+    if (s == "self") return self_block();
+    if (s.rfind("surface:", 0) == 0) return shared_surface(std::stoi(s.substr(8)));
+    if (s == "vertex") return shared_surface(0);
+    throw std::invalid_argument("unknown interaction: " + s);
+  }
+};
+
+enum class PointMode { Uniform = HB_POINTS_UNIFORM, GridInterior = HB_POINTS_GRID_INTERIOR,
+                       GridClosed = HB_POINTS_GRID_CLOSED };
+
+// SPEC pair_geometry: target cube [0,1]^d; source = target + o with
+// o = (2,0,..,0) far-field or d-d' leading ones for a d'-dimensional shared surface.
+struct PairGeometry {
+  int d = 1;
+  InteractionClass interaction;
+  HyperCube target, source;
+  int64_t n = 0;
+  PointMode mode = PointMode::Uniform;
+  uint64_t seed = 0;
+  hb_pair to_c() const {
+    hb_pair p{};
+    p.target = target.to_c();
+    p.source = source.to_c();
+    p.d_prime = interaction.is_far() ? -1 : interaction.surface_dim;
+    p.point_mode = static_cast<int32_t>(mode);
+    p.n_target = n;
+    p.n_source = n;
+    p.seed = seed;
+    return p;
+  }
+};
+
+inline PairGeometry pair_geometry(int d, InteractionClass inter, int64_t n,
+                                  PointMode mode = PointMode::Uniform, uint64_t seed = 0) {
+  if (d < 1 || d > 8) throw std::invalid_argument("pair_geometry: 1 <= d <= 8");
+  if (inter.kind == InteractionClass::Kind::SelfBlock)
+    throw std::invalid_argument("pair_geometry: self interaction is not a cube pair");
+  if (!inter.is_far() && (inter.surface_dim < 0 || inter.surface_dim > d - 1))
+    throw std::invalid_argument("pair_geometry: invalid d'");
+  std::vector<double> o(d, 0.0);
+  if (inter.is_far()) o[0] = 2.0;
+  else
+    for (int k = 0; k < d - inter.surface_dim; ++k) o[k] = 1.0;
+  PairGeometry g;
+  g.d = d;
+  g.interaction = inter;
+  g.target = HyperCube(std::vector<double>(d, 0.0), 1.0);
+  g.source = HyperCube(o, 1.0);
+  g.n = n;
+  g.mode = mode;
+  g.seed = seed;
+  return g;
+}
+
+inline uint64_t problem_seed(uint64_t base, int d, const InteractionClass& inter, int64_t n) {
+  return hb_problem_seed(base, d, inter.is_far() ? -1 : inter.surface_dim, n);
+}
+
+// SPEC RankRecord + certification data.
+struct RankRecord {
+  std::string kernel;
+  int d = 0;
+  InteractionClass interaction;
+  int64_t N = 0;
+  double epsilon = 0.0;
+  int rank = 0;
+  int rank_lo = 0, rank_hi = 0, k_factored = 0;
+  double sigma1 = 0.0, sigma_r = 0.0, sigma_r1 = 0.0, gap = 0.0;
+  double seconds = 0.0;
+};
+
+// RAII device context (one per device and host thread).
+class Device {
+ public:
+  explicit Device(int device = 0) { check(hb_context_create(device, &ctx_), "hb_context_create"); }
+  ~Device() { hb_context_destroy(ctx_); }
+  Device(const Device&) = delete;
+  Device& operator=(const Device&) = delete;
+  hb_context* get() const { return ctx_; }
+
+ private:
+  hb_context* ctx_ = nullptr;
+};
+
+// SPEC epsilon_rank of one generated block: count of σ_k > eps·σ₁.
+inline std::vector<RankRecord> epsilon_rank(Device& dev, const KernelSpec& k, const PairGeometry& g,
+                                            const std::vector<double>& eps) {
+  if (eps.empty() || eps.size() > HB_MAX_TOLS) throw std::invalid_argument("need 1..4 tolerances");
+  const hb_kernel ck = k.to_c();
+  const hb_pair cp = g.to_c();
+  std::vector<hb_rank_result> out(eps.size());
+  check(hb_rank(dev.get(), &ck, &cp, eps.data(), (int32_t)eps.size(), out.data()), "epsilon_rank",
+        dev.get());
+  std::vector<RankRecord> recs;
+  for (size_t t = 0; t < eps.size(); ++t) {
+    RankRecord r;
+    r.kernel = kernel_name(k); r.d = g.d; r.interaction = g.interaction; r.N = g.n;
+    r.epsilon = eps[t]; r.rank = out[t].rank; r.rank_lo = out[t].rank_lo; r.rank_hi = out[t].rank_hi;
+    r.k_factored = out[t].k_factored; r.sigma1 = out[t].sigma1; r.sigma_r = out[t].sigma_r;
+    r.sigma_r1 = out[t].sigma_r1; r.gap = out[t].gap; r.seconds = out[t].sec[3];
+    recs.push_back(r);
+  }
+  return recs;
+}
+
+// SPEC epsilon_rank(matrix, epsilon) on a device matrix (column-major m x n, leading dim ld).
+inline int epsilon_rank(Device& dev, const double* d_matrix, int64_t m, int64_t n, int64_t ld,
+                        double eps) {
+  hb_rank_result r{};
+  check(hb_rank_matrix(dev.get(), d_matrix, m, n, ld, &eps, 1, &r), "epsilon_rank", dev.get());
+  return r.rank;
+}
+
+// SPEC rank_table: one record per (kernel, N), problems spread over the
+// given devices by hb_sweep (LPT partition, one worker thread per device).
+inline std::vector<RankRecord> rank_table(const std::vector<KernelSpec>& kernels,
+                                          const InteractionClass& inter, int d,
+                                          const std::vector<int64_t>& n_list, double epsilon,
+                                          const std::vector<int>& devices = {0},
+                                          PointMode mode = PointMode::Uniform, uint64_t base_seed = 0,
+                                          std::vector<hb_status>* statuses = nullptr) {
+  std::vector<hb_problem> probs;
+  std::vector<RankRecord> recs;
+  for (const auto& k : kernels)
+    for (int64_t n : n_list) {
+      const uint64_t seed = mode == PointMode::Uniform ? problem_seed(base_seed, d, inter, n) : base_seed;
+      const PairGeometry g = pair_geometry(d, inter, n, mode, seed);
+      hb_problem p{};
+      p.kernel = k.to_c();
+      p.pair = g.to_c();
+      p.tols[0] = epsilon;
+      p.ntol = 1;
+      probs.push_back(p);
+      RankRecord r;
+      r.kernel = kernel_name(k); r.d = d; r.interaction = inter; r.N = n; r.epsilon = epsilon;
+      recs.push_back(r);
+    }
+  std::vector<hb_rank_result> out(probs.size());
+  std::vector<int32_t> st(probs.size(), 0);
+  std::vector<int32_t> devs(devices.begin(), devices.end());
+  hb_sweep(probs.data(), (int64_t)probs.size(), devs.data(), (int32_t)devs.size(), out.data(), st.data());
+  for (size_t i = 0; i < probs.size(); ++i) {
+    auto& r = recs[i];
+    r.rank = out[i].rank; r.rank_lo = out[i].rank_lo; r.rank_hi = out[i].rank_hi;
+    r.k_factored = out[i].k_factored; r.sigma1 = out[i].sigma1; r.sigma_r = out[i].sigma_r;
+    r.sigma_r1 = out[i].sigma_r1; r.gap = out[i].gap; r.seconds = out[i].sec[3];
+    if (statuses) statuses->push_back(static_cast<hb_status>(st[i]));
+  }
+  return recs;
+}
+
+// CSV schema of SPEC.md:613 (+ certification columns).
+inline void write_csv_header(std::ostream& os) {
+  os << "kernel,d,interaction,dprime,N,epsilon,rank,seconds,rank_lo,rank_hi,k_factored,sigma1,gap\n";
+}
+inline void write_csv_row(std::ostream& os, const RankRecord& r) {
+  os << r.kernel << ',' << r.d << ',' << r.interaction.name() << ','
+     << (r.interaction.is_far() ? -1 : r.interaction.surface_dim) << ',' << r.N << ',' << r.epsilon
+     << ',' << r.rank << ',' << r.seconds << ',' << r.rank_lo << ',' << r.rank_hi << ','
+     << r.k_factored << ',' << r.sigma1 << ',' << r.gap << '\n';
+}
+
+}  // namespace hb200

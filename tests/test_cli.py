@@ -1,0 +1,37 @@
+"""SPEC cli `rank-bench` built on the C++ host mirror (host/hb200.hpp)."""
+import subprocess
+
+import pytest
+
+from conftest import ROOT
+
+EXE = ROOT / "paper_2209_05819_b200" / "lib" / "rank-bench"
+
+
+def run(*args):
+    return subprocess.run([str(EXE), *args], capture_output=True, text=True, timeout=600)
+
+
+def test_cli_usage_errors():
+    if not EXE.exists():
+        pytest.skip("rank-bench not built")
+    assert run("--d", "1").returncode == 64                       # missing required flag
+    assert run("--d", "1", "--interaction", "far", "--kernel", "nope", "--N", "10").returncode == 64
+    assert run("--d", "1", "--interaction", "far", "--kernel", "log_r", "--N", "10",
+               "--grid", "weird").returncode == 64
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("args,want", [
+    (["--d", "1", "--interaction", "far", "--kernel", "log_r", "--N", "1000", "--grid", "closed"], 7),
+    (["--d", "2", "--interaction", "surface:0", "--kernel", "one_over_r", "--N", "10000",
+      "--grid", "interior"], 104),  # SPEC.md:637 example (paper 2D vertex F1, N=10000)
+    (["--d", "3", "--interaction", "surface:2", "--kernel", "one_over_r", "--N", "1000",
+      "--grid", "interior"], 312),
+])
+def test_cli_paper_values(args, want):
+    r = run(*args)
+    assert r.returncode == 0, r.stderr
+    lines = r.stdout.strip().splitlines()
+    assert lines[0].startswith("kernel,d,interaction,dprime,N,epsilon,rank,seconds")
+    assert int(lines[1].split(",")[6]) == want

@@ -139,7 +139,7 @@ def test_full_size_properties(ctx, hb, d, dp, kname, n):
     r = ctx.rank(k, pair, [1e-12, 1e-10, 1e-8])
     assert all(x.rank_lo == x.rank_hi for x in r)                 # certified bracket
     assert r[0].rank >= r[1].rank >= r[2].rank                    # non-increasing in ε
-    assert r[0].resid <= 0.01 * 1e-12 * r[0].sigma1 * 1.0001      # stopping rule held
+    assert r[0].resid <= 0.05 * 1e-12 * r[0].sigma1 * 1.0001      # stopping rule held (eta 0.05)
     rt = ctx.rank(k, pair, [1e-12])[0]
     assert rt.rank == r[0].rank and rt.sigma1 == r[0].sigma1      # deterministic
 

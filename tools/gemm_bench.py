@@ -1,0 +1,34 @@
+"""Time the FP64 DMMA GEMM (include/hb_debug.h hook) on the rank-reveal shapes.
+Usage: python tools/gemm_bench.py [reps]"""
+import sys
+
+import torch
+
+sys.path.insert(0, ".")
+import paper_2209_05819_b200 as hb  # noqa: E402
+
+reps = int(sys.argv[1]) if len(sys.argv) > 1 else 5
+SHAPES = [  # (transA, M, N, K, beta): name
+    ((0, 8192, 8192, 8192, 1.0), "square 8192^3"),
+    ((0, 32768, 32768, 120, 1.0), "trailing update A2 -= V W (K=b=120)"),
+    ((1, 120, 32768, 32768, 0.0), "W = V^T A2 (TN reduce, M=b)"),
+    ((0, 128, 65536, 65536, 0.0), "sketch Y = Omega A (M=128)"),
+    ((0, 16384, 16384, 32, 1.0), "band-reduction update (K=32)"),
+]
+ctx = hb.Context(0)
+s = torch.cuda.ExternalStream(ctx.stream)
+for (ta, M, N, K, beta), name in SHAPES:
+    A = torch.randn((M * K,), dtype=torch.float64, device="cuda")
+    B = torch.randn((K * N,), dtype=torch.float64, device="cuda")
+    C = torch.randn((M * N,), dtype=torch.float64, device="cuda")
+    lda = K if ta else M
+    torch.cuda.synchronize()
+    ctx.dgemm(bool(ta), M, N, K, 1.0, A.data_ptr(), lda, B.data_ptr(), K, beta, C.data_ptr(), M, reps=1)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(s)
+    ctx.dgemm(bool(ta), M, N, K, 1.0, A.data_ptr(), lda, B.data_ptr(), K, beta, C.data_ptr(), M, reps=reps)
+    e1.record(s)
+    e1.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    print(f"{name:45s} {M}x{N}x{K}: {ms:8.3f} ms {2 * M * N * K / ms / 1e9:7.2f} TF/s", flush=True)
+    del A, B, C
