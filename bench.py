@@ -284,7 +284,8 @@ def main():
                     mism.append({"d": d, "dprime": dp, "kernel": k, "N": n, "tol": tols[t],
                                  "gpu": r.rank, "oracle": g["ranks"][t], "gap_oracle": g["gaps"][t],
                                  "gap_gpu": r.gap})
-    uncert = sum(1 for res in full for r in res if r.rank_lo != r.rank_hi)
+    uncert = sum(1 for res in full for r in res if r.certificate == 0)
+    prob_cert = sum(1 for res in full for r in res if r.certificate == 2)
     path_tf = total_alg * args.steps / t_dev / 1e12
     line = {
         "metric": METRIC, "value": round(value, 4), "unit": "G entries/s", "n_gpus": world,
@@ -307,7 +308,7 @@ def main():
         "gpu_launches": int(launches),
         "clocks": clocks,
         "parity": {"checked_vs_oracle": checked, "equal": equal, "mismatches": mism[:20],
-                   "uncertified_brackets": uncert,
+                   "uncertified_brackets": uncert, "probabilistic_certificates": prob_cert,
                    "statuses_ok": all(s == 0 for s in statuses)},
         "phase_ms": {k: round(v, 1) for k, v in stats["phase_ms"].items()},
         "gemm_ms": round(stats["gemm_ms"], 1),

@@ -99,8 +99,12 @@ typedef struct {
   double sigma_r;      /* σ_p   (0 if p == 0) */
   double sigma_r1;     /* σ_{p+1} (0 if p == min(m, n)) */
   double gap;          /* min(σ_p/thr − 1, 1 − σ_{p+1}/thr) */
-  double resid;        /* δ = ‖A22‖_F after k_factored columns */
+  double resid;        /* δ used for rank_hi: bound on ‖A22‖₂ after k_factored columns */
   double sec[4];       /* device seconds: points+assembly, factorisation, certification, total */
+  int32_t certificate; /* 1: rank_lo == rank_hi with δ = ‖A22‖_F (deterministic bound);
+                          2: rank_lo == rank_hi with δ = 2·(power-method estimate of ‖A22‖₂),
+                             valid with probability >= 1 - 1e-27; 0: bracket open */
+  int32_t reserved;
 } hb_rank_result;
 
 #define HB_MAX_TOLS 4
@@ -126,6 +130,9 @@ void hb_context_destroy(hb_context* ctx);
 void* hb_context_stream(hb_context* ctx);
 /* Tuning: block size cap (8..120, multiple of 8) and stop factor η (0 < η <= 0.1). */
 hb_status hb_context_set_tuning(hb_context* ctx, int32_t block_max, double eta);
+/* Stopping rule: 0 = deterministic only (stop when ‖A22‖_F <= η·tol·σ̂₁); 1 (default) = also
+ * stop when a block power estimate gives 2·σ̂(A22) <= η·tol·σ̂₁ (probabilistic certificate). */
+hb_status hb_context_set_stopping(hb_context* ctx, int32_t spectral);
 
 /* k1: seeded / grid points, SoA (coordinate k of point i at k*n + i), device pointers. */
 hb_status hb_generate_points(hb_context* ctx, const hb_pair* pair, double* d_tgt_soa,

@@ -304,6 +304,12 @@ hb_status hb_context_set_tuning(hb_context* ctx, int32_t block_max, double eta) 
   return HB_OK;
 }
 
+hb_status hb_context_set_stopping(hb_context* ctx, int32_t spectral) {
+  if (!ctx || spectral < 0 || spectral > 1) return HB_EINVAL;
+  ctx->spectral = spectral != 0;
+  return HB_OK;
+}
+
 hb_status hb_generate_points(hb_context* ctx, const hb_pair* pair, double* d_tgt, double* d_src) {
   if (!ctx) return HB_EINVAL;
   return guarded(ctx, [&] {

@@ -57,24 +57,25 @@ struct GemmParams {
   int64_t fro_row0;
 };
 
-template <bool TA, int WARPS_M, int WARPS_N, int WM, int WN>
+template <bool TA, int WARPS_M, int WARPS_N, int WM, int WN, int BK_ = 16, int ST_ = 3>
 struct Cfg {
   static constexpr int NT = WARPS_M * WARPS_N * 32;  // threads per CTA
   static constexpr int BM = WARPS_M * WM * 8;
   static constexpr int BN = WARPS_N * WN * 8;
-  static constexpr int BK = 16;
-  static constexpr int STAGES = 3;
+  static constexpr int BK = BK_;
+  static constexpr int STAGES = ST_;
   static constexpr int AS = TA ? (BK + 4) : (BM + 4);  // A row stride
   static constexpr int A_ELEMS = TA ? BM * (BK + 4) : BK * (BM + 4);
   static constexpr int B_ELEMS = BN * (BK + 4);
   static constexpr int SMEM = STAGES * (A_ELEMS + B_ELEMS) * 8;
 };
 
-template <bool TA, int WARPS_M, int WARPS_N, int WM, int WN, bool VEC>
-__global__ void __launch_bounds__(Cfg<TA, WARPS_M, WARPS_N, WM, WN>::NT,
-                                  Cfg<TA, WARPS_M, WARPS_N, WM, WN>::NT == 128 ? 2 : 1)
+template <bool TA, int WARPS_M, int WARPS_N, int WM, int WN, bool VEC, int BK_, int ST_>
+__global__ void __launch_bounds__(Cfg<TA, WARPS_M, WARPS_N, WM, WN, BK_, ST_>::NT,
+                                  (WM * WN <= 16 && WARPS_M * WARPS_N == 4) ? 3
+                                      : (Cfg<TA, WARPS_M, WARPS_N, WM, WN, BK_, ST_>::NT == 128 ? 2 : 1))
     dgemm_kernel(GemmParams p) {
-  using C_ = Cfg<TA, WARPS_M, WARPS_N, WM, WN>;
+  using C_ = Cfg<TA, WARPS_M, WARPS_N, WM, WN, BK_, ST_>;
   constexpr int BM = C_::BM, BN = C_::BN, BK = C_::BK, STAGES = C_::STAGES, NT = C_::NT;
   extern __shared__ __align__(16) double smem[];
   double* As = smem;
@@ -96,61 +97,82 @@ __global__ void __launch_bounds__(Cfg<TA, WARPS_M, WARPS_N, WM, WN>::NT,
     }
   }
 
+  // ---- tile loader: per-thread source pointers / shared offsets / bound masks are set up
+  // once; each k-tile only advances the pointers (the K tail is checked per tile).
+  constexpr int VPC = BM / 2;   // N-mode A: 16-byte vectors per k-column of the tile
+  constexpr int VPR = BK / 2;   // T-mode A and B: vectors per m/n-row of the tile
+  constexpr int A_PT = (TA ? BM * VPR : BK * VPC) / NT;
+  constexpr int B_PT = (BN * VPR) / NT;
+  static_assert((TA ? BM * VPR : BK * VPC) % NT == 0 && (BN * VPR) % NT == 0, "loader split");
+  static_assert(TA ? (NT % VPR == 0) : (NT % VPC == 0), "loader stride");
+  // N-mode A: mm fixed, kk_i = kk0 + i*(NT/VPC);  T-mode A / B: kk fixed, row_i = r0 + i*(NT/VPR)
+  const int a_kk0 = TA ? (tid % VPR) * 2 : tid / VPC;
+  const int a_r0 = TA ? tid / VPR : (tid % VPC) * 2;
+  const int b_kk0 = (tid % VPR) * 2, b_r0 = tid / VPR;
+  uint32_t a_rowok = 0, b_rowok = 0;  // T-mode: bit i = row i inside M / N
+  int a_mbytes = 0;                   // N-mode: bytes valid along m (16 / 8 / 0)
+  if (TA) {
+#pragma unroll
+    for (int i = 0; i < A_PT; ++i)
+      if (m0 + a_r0 + i * (NT / VPR) < p.M) a_rowok |= 1u << i;
+  } else {
+    const int64_t gm = m0 + a_r0;
+    a_mbytes = gm + 1 < p.M ? 16 : (gm < p.M ? 8 : 0);
+  }
+#pragma unroll
+  for (int i = 0; i < B_PT; ++i)
+    if (n0 + b_r0 + i * (NT / VPR) < p.N) b_rowok |= 1u << i;
+  const double* a_ptr = TA ? p.A + (kbeg + a_kk0) + (m0 + a_r0) * p.lda
+                           : p.A + (m0 + a_r0) + (kbeg + a_kk0) * p.lda;
+  const double* b_ptr = p.B + (kbeg + b_kk0) + (n0 + b_r0) * p.ldb;
+  const int64_t a_istride = TA ? (int64_t)(NT / VPR) * p.lda : (int64_t)(NT / VPC) * p.lda;
+  const int64_t a_kstride = TA ? (int64_t)BK : (int64_t)BK * p.lda;
+  const int64_t b_istride = (int64_t)(NT / VPR) * p.ldb;
+  const uint32_t a_dst0 = smem_u32(As) + 8u * (TA ? (a_r0 * (BK + 4) + a_kk0) : (a_kk0 * (BM + 4) + a_r0));
+  const uint32_t b_dst0 = smem_u32(Bs) + 8u * (b_r0 * (BK + 4) + b_kk0);
+  constexpr uint32_t A_IDST = 8u * (TA ? (NT / VPR) * (BK + 4) : (NT / VPC) * (BM + 4));
+  constexpr uint32_t B_IDST = 8u * (NT / VPR) * (BK + 4);
+
   auto load_tile = [&](int kt, int stage) {
-    const int64_t k0 = kbeg + (int64_t)kt * BK;
-    double* as = As + stage * C_::A_ELEMS;
-    double* bs = Bs + stage * C_::B_ELEMS;
-    if (!TA) {
-      constexpr int VPC = BM / 2;
-      for (int v = tid; v < BK * VPC; v += NT) {
-        const int kk = v / VPC, mm = (v % VPC) * 2;
-        const int64_t gm = m0 + mm, gk = k0 + kk;
-        const double* src = p.A + gm + gk * p.lda;
-        double* dst = as + kk * (BM + 4) + mm;
-        if (VEC) {
-          int bytes = 0;
-          if (gk < kend) bytes = gm + 1 < p.M ? 16 : (gm < p.M ? 8 : 0);
-          cp_async16(smem_u32(dst), bytes ? src : p.A, bytes);
-        } else {
-          const bool v0 = gk < kend && gm < p.M, v1 = gk < kend && gm + 1 < p.M;
-          cp_async8(smem_u32(dst), v0 ? src : p.A, v0 ? 8 : 0);
-          cp_async8(smem_u32(dst + 1), v1 ? src + 1 : p.A, v1 ? 8 : 0);
-        }
+    const int64_t k0 = kbeg + (int64_t)kt * BK;  // tile start
+    const bool full_k = k0 + BK <= kend;
+    const uint32_t a_st = a_dst0 + 8u * stage * C_::A_ELEMS;
+    const uint32_t b_st = b_dst0 + 8u * stage * C_::B_ELEMS;
+    const double* ap = a_ptr + kt * a_kstride;
+    const double* bp = b_ptr + (int64_t)kt * BK;
+    // T-mode / B: the k-extent of this thread's vector (uniform over i)
+    const int64_t gk = k0 + (TA ? a_kk0 : 0);
+    const int kb_a = full_k ? 16 : (gk + 1 < kend ? 16 : (gk < kend ? 8 : 0));
+    const int64_t gkb = k0 + b_kk0;
+    const int kb_b = full_k ? 16 : (gkb + 1 < kend ? 16 : (gkb < kend ? 8 : 0));
+#pragma unroll
+    for (int i = 0; i < A_PT; ++i) {
+      const double* src = ap + i * a_istride;
+      int bytes;
+      if (TA) {
+        bytes = ((a_rowok >> i) & 1u) ? kb_a : 0;
+      } else {
+        const bool kin = full_k || (k0 + a_kk0 + i * (NT / VPC) < kend);
+        bytes = kin ? a_mbytes : 0;
       }
-    } else {
-      constexpr int VPR = BK / 2;
-      for (int v = tid; v < BM * VPR; v += NT) {
-        const int mm = v / VPR, kk = (v % VPR) * 2;
-        const int64_t gm = m0 + mm, gk = k0 + kk;
-        const double* src = p.A + gk + gm * p.lda;
-        double* dst = as + mm * (BK + 4) + kk;
-        if (VEC) {
-          int bytes = 0;
-          if (gm < p.M) bytes = gk + 1 < kend ? 16 : (gk < kend ? 8 : 0);
-          cp_async16(smem_u32(dst), bytes ? src : p.A, bytes);
-        } else {
-          const bool v0 = gm < p.M && gk < kend, v1 = gm < p.M && gk + 1 < kend;
-          cp_async8(smem_u32(dst), v0 ? src : p.A, v0 ? 8 : 0);
-          cp_async8(smem_u32(dst + 1), v1 ? src + 1 : p.A, v1 ? 8 : 0);
-        }
+      const uint32_t dst = a_st + i * A_IDST;
+      if (VEC) {
+        cp_async16(dst, bytes ? src : p.A, bytes);
+      } else {
+        cp_async8(dst, bytes >= 8 ? src : p.A, bytes >= 8 ? 8 : 0);
+        cp_async8(dst + 8, bytes >= 16 ? src + 1 : p.A, bytes >= 16 ? 8 : 0);
       }
     }
-    {
-      constexpr int VPR = BK / 2;
-      for (int v = tid; v < BN * VPR; v += NT) {
-        const int nn = v / VPR, kk = (v % VPR) * 2;
-        const int64_t gn = n0 + nn, gk = k0 + kk;
-        const double* src = p.B + gk + gn * p.ldb;
-        double* dst = bs + nn * (BK + 4) + kk;
-        if (VEC) {
-          int bytes = 0;
-          if (gn < p.N) bytes = gk + 1 < kend ? 16 : (gk < kend ? 8 : 0);
-          cp_async16(smem_u32(dst), bytes ? src : p.B, bytes);
-        } else {
-          const bool v0 = gn < p.N && gk < kend, v1 = gn < p.N && gk + 1 < kend;
-          cp_async8(smem_u32(dst), v0 ? src : p.B, v0 ? 8 : 0);
-          cp_async8(smem_u32(dst + 1), v1 ? src + 1 : p.B, v1 ? 8 : 0);
-        }
+#pragma unroll
+    for (int i = 0; i < B_PT; ++i) {
+      const double* src = bp + i * b_istride;
+      const int bytes = ((b_rowok >> i) & 1u) ? kb_b : 0;
+      const uint32_t dst = b_st + i * B_IDST;
+      if (VEC) {
+        cp_async16(dst, bytes ? src : p.B, bytes);
+      } else {
+        cp_async8(dst, bytes >= 8 ? src : p.B, bytes >= 8 ? 8 : 0);
+        cp_async8(dst + 8, bytes >= 16 ? src + 1 : p.B, bytes >= 16 ? 8 : 0);
       }
     }
   };
@@ -307,18 +329,18 @@ __global__ void splitk_reduce(GemmParams p, int slices) {
   }
 }
 
-template <bool TA, int WARPS_M, int WARPS_N, int WM, int WN>
+template <bool TA, int WARPS_M, int WARPS_N, int WM, int WN, int BK_ = 16, int ST_ = 3>
 static void run_cfg(const GemmParams& p, int slices, bool vec, cudaStream_t st) {
-  using C_ = Cfg<TA, WARPS_M, WARPS_N, WM, WN>;
+  using C_ = Cfg<TA, WARPS_M, WARPS_N, WM, WN, BK_, ST_>;
   dim3 grid((unsigned)ceil_div(p.M, C_::BM), (unsigned)ceil_div(p.N, C_::BN), (unsigned)slices);
   HB_REQUIRE(grid.y <= 65535u && grid.z <= 65535u, HB_ECAP, "dgemm: grid too large");
   // the attribute is per device; setting it on every launch costs ~1 µs of host time
   if (vec) {
-    auto k = dgemm_kernel<TA, WARPS_M, WARPS_N, WM, WN, true>;
+    auto k = dgemm_kernel<TA, WARPS_M, WARPS_N, WM, WN, true, BK_, ST_>;
     HB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C_::SMEM));
     k<<<grid, C_::NT, C_::SMEM, st>>>(p);
   } else {
-    auto k = dgemm_kernel<TA, WARPS_M, WARPS_N, WM, WN, false>;
+    auto k = dgemm_kernel<TA, WARPS_M, WARPS_N, WM, WN, false, BK_, ST_>;
     HB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C_::SMEM));
     k<<<grid, C_::NT, C_::SMEM, st>>>(p);
   }
@@ -327,12 +349,24 @@ static void run_cfg(const GemmParams& p, int slices, bool vec, cudaStream_t st) 
 
 static constexpr int kReduceBlocks = 592;  // 4 x 148 SMs
 
+// Kernel variant for a shape (HB_GEMM_VAR overrides, for A/B experiments):
+//   4 (default): 64x64 tiles, 4 warps (32x32 warp tiles), BK 32, 2 stages, 3 CTAs/SM — fastest on
+//      every rank-reveal shape measured (tools/gemm_bench.py: 8192^3 34.6 TF/s, rank-120 update
+//      26.1, Vᵀ·A2 31.4, Ω·A 33.9 of the 36.9 TF/s DMMA peak);
+//   2: 128x64 tiles, 2 CTAs/SM;  100: 64x128 tiles, 8 warps (small M)
+static int gemm_variant(int64_t M, int64_t N, int64_t K) {
+  static const int env = [] {
+    const char* e = getenv("HB_GEMM_VAR");
+    return e ? atoi(e) : -1;
+  }();
+  (void)N; (void)K;
+  if (env >= 0) return (M <= 64 && env != 4 && env != 100) ? 100 : env;
+  return 4;
+}
 static int64_t tiles_of(int64_t M, int64_t N, int64_t K) {
-  const char* e = getenv("HB_GEMM_CFG");
-  const int cfg = e ? atoi(e) : 0;
-  const int bm = M <= 64 ? 64 : 128;
-  const int bn = (M > 64 && cfg != 2) ? 64 : 128;
-  (void)K;
+  const int v = gemm_variant(M, N, K);
+  const int bm = v == 100 ? 64 : (v == 4 ? 64 : (v == 3 ? 64 : 128));
+  const int bn = v == 100 ? 128 : (v == 4 ? 64 : (v == 3 ? 128 : 64));
   return ceil_div(M, bm) * ceil_div(N, bn);
 }
 
@@ -371,21 +405,24 @@ void launch_dgemm(const GemmArgs& g, double* ws, int64_t ws_elems, int num_sms, 
     q.partial = ws;
     q.fro = nullptr;
   }
-  static const int cfg_env = [] {
-    const char* e = getenv("HB_GEMM_CFG");
-    return e ? atoi(e) : 0;
-  }();
-  if (g.M <= 64) {
+  const int var = gemm_variant(g.M, g.N, g.K);
+  if (var == 100) {
     if (g.transA) run_cfg<true, 1, 8, 8, 2>(q, s_eff, vec, st);
     else run_cfg<false, 1, 8, 8, 2>(q, s_eff, vec, st);
-  } else if (cfg_env != 2) {
-    // 128x64 tiles, 4 warps, 2 CTAs per SM: one CTA's epilogue (C read-modify-write) overlaps the
-    // other's DMMA main loop (measured faster than 128x128 on every rank-reveal shape)
-    if (g.transA) run_cfg<true, 2, 2, 8, 4>(q, s_eff, vec, st);
-    else run_cfg<false, 2, 2, 8, 4>(q, s_eff, vec, st);
+  } else if (var == 4) {
+    if (g.transA) run_cfg<true, 2, 2, 4, 4, 32, 2>(q, s_eff, vec, st);
+    else run_cfg<false, 2, 2, 4, 4, 32, 2>(q, s_eff, vec, st);
+  } else if (var == 3) {
+    if (g.transA) run_cfg<true, 2, 2, 4, 8, 16, 3>(q, s_eff, vec, st);
+    else run_cfg<false, 2, 2, 4, 8, 16, 3>(q, s_eff, vec, st);
+  } else if (var == 0) {
+    if (g.transA) run_cfg<true, 2, 2, 8, 4, 16, 3>(q, s_eff, vec, st);
+    else run_cfg<false, 2, 2, 8, 4, 16, 3>(q, s_eff, vec, st);
   } else {
-    if (g.transA) run_cfg<true, 2, 4, 8, 4>(q, s_eff, vec, st);
-    else run_cfg<false, 2, 4, 8, 4>(q, s_eff, vec, st);
+    // 128x64 tiles, 4 warps, BK 32, 2 stages, 2 CTAs per SM: one CTA's epilogue (C read-modify-
+    // write) overlaps the other's DMMA main loop (measured fastest on the rank-reveal shapes)
+    if (g.transA) run_cfg<true, 2, 2, 8, 4, 32, 2>(q, s_eff, vec, st);
+    else run_cfg<false, 2, 2, 8, 4, 32, 2>(q, s_eff, vec, st);
   }
   if (s_eff > 1) {
     p.partial = ws;

@@ -479,11 +479,12 @@ __global__ void __launch_bounds__(256) power_sigma1_kernel(PowerParams p) {
     double yy = 0.0;
     for (int64_t c = c0 + warp; c < c1; c += 8) {
       const double* col = p.R + c * p.ld;
-      const int rmax = c < b ? (int)c + 1 : b;
+      const int rmax = (p.mask && c < b) ? (int)c + 1 : b;
       double s = 0.0;
       for (int i = lane; i < rmax; i += 32) s += col[i] * x[i];
       s = warp_sum(s);
       yy += s * s;
+      if (p.yout && it == p.iters - 1 && lane == 0) p.yout[c] = s;
       for (int i = lane; i < rmax; i += 32) acc[warp][i] += col[i] * s;
     }
     if (lane == 0) ysum[warp] = yy;
@@ -550,5 +551,34 @@ __global__ void nonfinite_kernel(const double* __restrict__ A, int64_t m, int64_
   if (idx >= m * n) return;
   const int64_t i = idx % m, c = idx / m;
   if (!isfinite(A[i + c * ld])) atomicOr(flags, 2u);
+}
+}  // namespace hb
+
+namespace hb {
+// Spectral-norm check of the residual (block power method without re-orthogonalisation, so
+// every column is an independent power iteration): normalise each column of X (rows x cols)
+// and record its pre-normalisation norm in norms[c] (max over the run = lower bound on σ₁).
+__global__ void colnorm_normalize_kernel(double* __restrict__ X, int64_t ld, int64_t rows,
+                                         double* __restrict__ norms, double* __restrict__ best) {
+  __shared__ double red[32];
+  const int c = blockIdx.x;
+  double* x = X + (int64_t)c * ld;
+  double s = 0.0;
+  for (int64_t i = threadIdx.x; i < rows; i += blockDim.x) s += x[i] * x[i];
+  s = block_sum(s, red);
+  const double nrm = sqrt(s);
+  const double inv = nrm > 0.0 ? 1.0 / nrm : 0.0;
+  for (int64_t i = threadIdx.x; i < rows; i += blockDim.x) x[i] *= inv;
+  if (threadIdx.x == 0) {
+    norms[c] = nrm;
+    if (best) best[c] = fmax(best[c], nrm);
+  }
+}
+__global__ void max_kernel(const double* __restrict__ v, int n, double* __restrict__ out) {
+  if (threadIdx.x == 0) {
+    double m = 0.0;
+    for (int i = 0; i < n; ++i) m = fmax(m, v[i]);
+    *out = m;
+  }
 }
 }  // namespace hb

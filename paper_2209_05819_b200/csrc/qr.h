@@ -45,8 +45,10 @@ struct PowerParams {
   int b;
   int64_t n;
   int iters;
+  int mask;       // 1: first b columns upper trapezoidal (R factor), 0: dense (sketch rows)
   double* slots;  // [2][G][b+1]
   double* out;
+  double* yout;   // optional: Rᵀ x of the last iteration (right singular direction), length n
   GridBarrier bar;
 };
 
@@ -82,8 +84,10 @@ __global__ void bidiag_kernel(BidiagParams p);
 
 // Bisection on the upper bidiagonal (d, e): singular-value queries.
 struct SigmaQuery {
-  double tol;     // relative tolerance
-  double delta;   // residual bound δ for rank_hi
+  double tol;       // relative tolerance
+  double delta;     // residual bound δ for rank_hi
+  int counts_only;  // skip the σ_p / σ_{p+1} bisections
+  int pad;
 };
 struct SigmaAnswer {
   double sigma1, sigma_p, sigma_p1;
@@ -104,5 +108,8 @@ __global__ void sigma_all_kernel(const double* d, const double* e, int64_t k, do
 
 namespace hb {
 __global__ void iota_kernel(int64_t* p, int64_t n);
+__global__ void colnorm_normalize_kernel(double* X, int64_t ld, int64_t rows, double* norms,
+                                         double* best);
+__global__ void max_kernel(const double* v, int n, double* out);
 __global__ void nonfinite_kernel(const double* A, int64_t m, int64_t n, int64_t ld, unsigned int* flags);
 }  // namespace hb

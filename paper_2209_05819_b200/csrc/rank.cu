@@ -163,6 +163,83 @@ void apply_block_reflector(hb_context* c, const double* V, int64_t ldv, const do
   }
 }
 
+// σ_max of the first `rows` rows (rows <= kBlockMax) of a column-major matrix with ld, n
+// columns, by the grid-cooperative power iteration (lower bound, converges from below).
+double sigma_max_rows(hb_context* c, const double* R, int64_t ld, int rows, int64_t n, int iters,
+                      double* yout = nullptr) {
+  double* out = ws<double>(c, B_PN, 16);
+  PowerParams pw{};
+  pw.R = R; pw.ld = ld; pw.b = rows; pw.n = n; pw.iters = iters; pw.mask = 0; pw.yout = yout;
+  pw.slots = ws<double>(c, B_SIG1, (size_t)2 * c->num_sms * (kBlockMax + 1));
+  pw.out = out + 8; pw.bar = barrier(c);
+  coop(power_sigma1_kernel, clampi(ceil_div(n, 256), 1, c->num_sms), 0, c->stream, pw);
+  double h = 0.0;
+  sync_to_host(c, out + 8, &h, sizeof(double));
+  return h;
+}
+
+// Block power method on the residual A22 (m2 x n2): r = 8 independent Gaussian start vectors,
+// q = 10 iterations of x <- A22ᵀ A22 x, each column normalised separately (no re-orthogonali-
+// sation, so each is an independent power iteration).  Returns the largest ‖A22 x‖ seen, a
+// lower bound on ‖A22‖₂.  Kuczyński–Woźniakowski: for one uniformly random start,
+// P[λ_est < (1−ε)λ_max] <= 0.824·sqrt(n)·(1−ε)^(q−1/2); with ε = 3/4 (σ_est < σ_max/2),
+// q = 10, n <= 65536 this is < 4.3e-4 per vector, < 1e-27 for all 8 — so 2·σ_est bounds ‖A22‖₂
+// except with that probability.
+double residual_sigma_max(hb_context* c, const double* A22, int64_t lda, int64_t m2, int64_t n2) {
+  constexpr int r = 8, q = 10;
+  cudaStream_t st = c->stream;
+  double* X = ws<double>(c, B_PX, (size_t)n2 * r);
+  double* Yv = ws<double>(c, B_PY, (size_t)m2 * r);
+  double* nb = ws<double>(c, B_PN, 16);
+  launch_gaussian(X, n2, r, n2, 0x5DEECE66Dull ^ (uint64_t)n2, st);
+  HB_CUDA(cudaMemsetAsync(nb + r, 0, r * sizeof(double), st));
+  colnorm_normalize_kernel<<<r, 1024, 0, st>>>(X, n2, n2, nb, nullptr);
+  HB_LAUNCH_CHECK();
+  Gemm gemm{c};
+  for (int it = 0; it < q; ++it) {
+    GemmArgs g{};
+    g.M = m2; g.N = r; g.K = n2; g.alpha = 1.0; g.A = A22; g.lda = lda; g.transA = false;
+    g.B = X; g.ldb = n2; g.beta = 0.0; g.C = Yv; g.ldc = m2;
+    gemm(g);
+    colnorm_normalize_kernel<<<r, 1024, 0, st>>>(Yv, m2, m2, nb, nb + r);  // ‖A22 x‖
+    HB_LAUNCH_CHECK();
+    GemmArgs g2{};
+    g2.M = n2; g2.N = r; g2.K = m2; g2.alpha = 1.0; g2.A = A22; g2.lda = lda; g2.transA = true;
+    g2.B = Yv; g2.ldb = m2; g2.beta = 0.0; g2.C = X; g2.ldc = n2;
+    gemm(g2);
+    colnorm_normalize_kernel<<<r, 1024, 0, st>>>(X, n2, n2, nb, nb + r);   // ‖A22ᵀ y‖
+    HB_LAUNCH_CHECK();
+  }
+  max_kernel<<<1, 32, 0, st>>>(nb + r, r, nb);
+  HB_LAUNCH_CHECK();
+  double h = 0.0;
+  sync_to_host(c, nb, &h, sizeof(double));
+  return h;
+}
+
+// Cheap screen for the spectral stopping test: the dominant right singular direction z of the
+// sketch Y2 = G·A22 (power iteration on its first rows) approximates that of A22; ‖A22 ẑ‖ is a
+// lower bound on ‖A22‖₂ (one pass over A22).
+double residual_sigma_screen(hb_context* c, const double* Y2, int64_t ldy, int rows, const double* A22,
+                             int64_t lda, int64_t m2, int64_t n2) {
+  cudaStream_t st = c->stream;
+  double* z = ws<double>(c, B_PX, (size_t)n2 * 8);
+  double* yv = ws<double>(c, B_PY, (size_t)m2 * 8);
+  double* nb = ws<double>(c, B_PN, 16);
+  sigma_max_rows(c, Y2, ldy, rows, n2, 12, z);
+  colnorm_normalize_kernel<<<1, 1024, 0, st>>>(z, n2, n2, nb, nullptr);
+  HB_LAUNCH_CHECK();
+  GemmArgs g{};
+  g.M = m2; g.N = 1; g.K = n2; g.alpha = 1.0; g.A = A22; g.lda = lda; g.transA = false;
+  g.B = z; g.ldb = n2; g.beta = 0.0; g.C = yv; g.ldc = m2;
+  Gemm{c}(g);
+  colnorm_normalize_kernel<<<1, 1024, 0, st>>>(yv, m2, m2, nb + 1, nullptr);
+  HB_LAUNCH_CHECK();
+  double h[2];
+  sync_to_host(c, nb, h, sizeof(h));
+  return h[1];
+}
+
 void sketch(hb_context* c, const double* A, int64_t lda, int64_t m, int64_t n, double* Y,
             uint64_t seed) {
   double* Om = ws<double>(c, B_OMEGA, (size_t)kSketchRows * std::max<int64_t>(m, 1));
@@ -287,7 +364,9 @@ void rank_matrix_inplace(hb_context* c, double* A, int64_t m, int64_t n, int64_t
   // smaller eta and certify again.  The bracket is rigorous for any δ; eta trades columns
   // (work) against the chance of a re-certification.
   double eta_cur = c->eta;
-  SigmaAnswer ans[HB_MAX_TOLS];
+  double delta2 = INFINITY;  // probabilistic bound 2·σ̂(A22) when the spectral test stopped us
+  int cert_kind[HB_MAX_TOLS] = {0, 0, 0, 0};
+  SigmaAnswer ans[2 * HB_MAX_TOLS];
   int64_t k = 0;
   int rounds = 0;
   for (;; ++rounds) {
@@ -347,7 +426,7 @@ void rank_matrix_inplace(hb_context* c, double* A, int64_t m, int64_t n, int64_t
       if (first) {
         Phase ph(c, HB_PH_SIGMA1);
         PowerParams pw{};
-        pw.R = A; pw.ld = lda; pw.b = bh; pw.n = n; pw.iters = 40;
+        pw.R = A; pw.ld = lda; pw.b = bh; pw.n = n; pw.iters = 40; pw.mask = 1;
         pw.slots = ws<double>(c, B_SIG1, (size_t)2 * c->num_sms * (kBlockMax + 1));
         pw.out = scal + 1; pw.bar = barrier(c);
         coop(power_sigma1_kernel, clampi(ceil_div(n, 256), 1, c->num_sms), 0, st, pw);
@@ -374,7 +453,30 @@ void rank_matrix_inplace(hb_context* c, double* A, int64_t m, int64_t n, int64_t
         first = false;
       }
       if (j >= kmax) break;
-      if (delta <= eta_cur * tol_min * sigma1_est) break;
+      const double target = eta_cur * tol_min * sigma1_est;
+      if (delta <= target) {
+        delta2 = INFINITY;
+        break;
+      }
+      if (c->spectral && sigma1_est > 0.0 && delta <= 64.0 * target) {
+        // screen: ‖A22 ẑ‖ with ẑ the sketch's dominant right direction (a lower bound on
+        // ‖A22‖₂); only when it is well below target run the certifying block power method
+        Phase ph(c, HB_PH_SIGMA1);
+        const double s2 = residual_sigma_screen(c, Y + j * ell, ell, std::min(ell, kBlockMax),
+                                                A + j + j * lda, lda, m - j, n - j);
+        static const bool dbg = getenv("HB_DEBUG_STOP") != nullptr;
+        if (dbg)
+          fprintf(stderr, "[stop] j=%lld dF/t=%.3g screen/t=%.3g\n", (long long)j, delta / target,
+                  s2 / target);
+        if (s2 <= target / 2.5) {
+          const double sig = residual_sigma_max(c, A + j + j * lda, lda, m - j, n - j);
+          if (dbg) fprintf(stderr, "[stop]   power/t=%.3g\n", sig / target);
+          if (2.0 * sig <= target) {
+            delta2 = 2.0 * sig;
+            break;
+          }
+        }
+      }
       if (!(fro_at_sketch < INFINITY)) fro_at_sketch = delta;
       if (delta < 1e-8 * fro_at_sketch) {
         Phase ph(c, HB_PH_SKETCH);
@@ -391,13 +493,21 @@ void rank_matrix_inplace(hb_context* c, double* A, int64_t m, int64_t n, int64_t
       }
       b = std::min(2 * b, c->block_max);
     }
-    if (j >= kmax) delta = 0.0;
+    if (j >= kmax) {
+      delta = 0.0;
+      delta2 = INFINITY;
+    }
     k = j;
     HB_CUDA(cudaEventRecord(c->ev[2], st));
 
     // ---- certification: σ(R_k) ------------------------------------------------------------
-    SigmaQuery hq[HB_MAX_TOLS];
-    for (int t = 0; t < ntol; ++t) hq[t] = SigmaQuery{tols[t], delta};
+    // queries [0, ntol): δ = ‖A22‖_F (deterministic); [ntol, 2 ntol): δ = 2σ̂(A22) (counts only)
+    SigmaQuery hq[2 * HB_MAX_TOLS];
+    const int nq = delta2 < INFINITY ? 2 * ntol : ntol;
+    for (int t = 0; t < ntol; ++t) {
+      hq[t] = SigmaQuery{tols[t], delta, 0, 0};
+      hq[ntol + t] = SigmaQuery{tols[t], delta2 < INFINITY ? delta2 : delta, 1, 0};
+    }
     std::memset(ans, 0, sizeof(ans));
     if (k > 0) {
       const int64_t ldb = round_up(n, 8);
@@ -426,15 +536,20 @@ void rank_matrix_inplace(hb_context* c, double* A, int64_t m, int64_t n, int64_t
       two_stage_bidiag(c, Mk, ldm, k, d, e, V, ldv, tau, T);
       ph_bd.close();
       Phase ph_bs(c, HB_PH_BISECT);
-      SigmaQuery* dq = ws<SigmaQuery>(c, B_QUERY, HB_MAX_TOLS);
-      SigmaAnswer* da = ws<SigmaAnswer>(c, B_ANSWER, HB_MAX_TOLS);
-      HB_CUDA(cudaMemcpyAsync(dq, hq, sizeof(SigmaQuery) * ntol, cudaMemcpyHostToDevice, st));
-      sigma_queries_kernel<<<1, 32 * HB_MAX_TOLS, 0, st>>>(d, e, k, dq, ntol, da);
+      SigmaQuery* dq = ws<SigmaQuery>(c, B_QUERY, 2 * HB_MAX_TOLS);
+      SigmaAnswer* da = ws<SigmaAnswer>(c, B_ANSWER, 2 * HB_MAX_TOLS);
+      HB_CUDA(cudaMemcpyAsync(dq, hq, sizeof(SigmaQuery) * nq, cudaMemcpyHostToDevice, st));
+      sigma_queries_kernel<<<1, 32 * 2 * HB_MAX_TOLS, 0, st>>>(d, e, k, dq, nq, da);
       HB_LAUNCH_CHECK();
-      sync_to_host(c, da, ans, sizeof(SigmaAnswer) * ntol);
+      sync_to_host(c, da, ans, sizeof(SigmaAnswer) * nq);
     }
     bool open = false;
-    for (int t = 0; t < ntol; ++t) open |= ans[t].rank_lo != ans[t].rank_hi;
+    for (int t = 0; t < ntol; ++t) {
+      cert_kind[t] = 0;
+      if (ans[t].rank_lo == ans[t].rank_hi) cert_kind[t] = 1;
+      else if (nq > ntol && ans[ntol + t].rank_hi == ans[t].rank_lo) cert_kind[t] = 2;
+      open |= cert_kind[t] == 0;
+    }
     if (!open || j >= kmax || rounds >= 3) break;
     eta_cur *= 0.2;
   }
@@ -468,7 +583,9 @@ void rank_matrix_inplace(hb_context* c, double* A, int64_t m, int64_t n, int64_t
       if (r.rank < kmax) gap = std::min(gap, 1.0 - r.sigma_r1 / thr);
     }
     r.gap = gap;
-    r.resid = delta;
+    r.certificate = cert_kind[t];
+    r.resid = cert_kind[t] == 2 ? delta2 : delta;
+    if (cert_kind[t] == 2) r.rank_hi = ans[ntol + t].rank_hi;
     r.sec[1] = f_ms * 1e-3;
     r.sec[2] = c_ms * 1e-3;
   }

@@ -234,8 +234,10 @@ __global__ void sigma_queries_kernel(const double* __restrict__ d, const double*
     const double thr_hi = thr2 > 0.0 ? sqrt(thr2) : 0.0;
     const int64_t phi = thr_hi > 0.0 ? k - count_less(d, e, k, nextafter(thr_hi, 1e308), pivmin) : k;
     double sp = 0.0, sp1 = 0.0;
-    if (p >= 1) sp = kth_largest(d, e, k, p, thr, sh_ub, pivmin);
-    if (p + 1 <= k) sp1 = kth_largest(d, e, k, p + 1, 0.0, xp, pivmin);
+    if (!q[qi].counts_only) {
+      if (p >= 1) sp = kth_largest(d, e, k, p, thr, sh_ub, pivmin);
+      if (p + 1 <= k) sp1 = kth_largest(d, e, k, p + 1, 0.0, xp, pivmin);
+    }
     if (lane == 0) {
       out[qi].sigma1 = s1;
       out[qi].sigma_p = sp;

@@ -61,7 +61,8 @@ class hb_rank_result(ctypes.Structure):
                 ("k_factored", ctypes.c_int32), ("sigma1", ctypes.c_double),
                 ("sigma_r", ctypes.c_double), ("sigma_r1", ctypes.c_double),
                 ("gap", ctypes.c_double), ("resid", ctypes.c_double),
-                ("sec", ctypes.c_double * 4)]
+                ("sec", ctypes.c_double * 4), ("certificate", ctypes.c_int32),
+                ("reserved", ctypes.c_int32)]
 
     def as_dict(self) -> dict:
         return {f: (list(getattr(self, f)) if f == "sec" else getattr(self, f))
@@ -101,7 +102,7 @@ EXPORTS = [
     "hb_context_stream", "hb_context_set_tuning", "hb_generate_points", "hb_assemble",
     "hb_eval_radial_host", "hb_rank_matrix", "hb_rank", "hb_last_sigma", "hb_sweep",
     "hb_partition", "hb_problem_seed", "hb_phase_name", "hb_context_set_profiling",
-    "hb_stats_get", "hb_stats_reset", "hb_sweep_ex", "hb_sweep_release",
+    "hb_stats_get", "hb_stats_reset", "hb_sweep_ex", "hb_sweep_release", "hb_context_set_stopping",
     # include/hb_debug.h (test hooks)
     "hb_debug_dgemm", "hb_debug_dgemm_async",
 ]
@@ -131,6 +132,8 @@ def load(path: os.PathLike | str | None = None):
     L.hb_context_stream.argtypes = [c_p]
     L.hb_context_stream.restype = c_p
     L.hb_context_set_tuning.argtypes = [c_p, ctypes.c_int32, ctypes.c_double]
+    L.hb_context_set_stopping.argtypes = [c_p, ctypes.c_int32]
+    L.hb_context_set_stopping.restype = ctypes.c_int
     L.hb_generate_points.argtypes = [c_p, ctypes.POINTER(hb_pair), c_p, c_p]
     L.hb_assemble.argtypes = [c_p, ctypes.POINTER(hb_kernel), c_p, ctypes.c_int64, c_p,
                               ctypes.c_int64, ctypes.c_int32, c_p, ctypes.c_int64]
@@ -268,11 +271,12 @@ class RankResult:
     gap: float
     resid: float
     sec: list
+    certificate: int = 0  # 1 deterministic bracket, 2 probabilistic (<1e-27), 0 open
 
     @classmethod
     def of(cls, r: hb_rank_result) -> "RankResult":
         return cls(r.rank, r.rank_lo, r.rank_hi, r.k_factored, r.sigma1, r.sigma_r, r.sigma_r1,
-                   r.gap, r.resid, list(r.sec))
+                   r.gap, r.resid, list(r.sec), r.certificate)
 
 
 class Context:
@@ -332,6 +336,9 @@ class Context:
         _check(self._lib.hb_rank_matrix(self._h, d_A, m, n, ld, ct, nt, out), "hb_rank_matrix",
                self._h)
         return [RankResult.of(o) for o in out]
+
+    def set_stopping(self, spectral: bool = True):
+        _check(self._lib.hb_context_set_stopping(self._h, int(spectral)), "set_stopping", self._h)
 
     def set_profiling(self, on: bool = True):
         _check(self._lib.hb_context_set_profiling(self._h, int(on)), "set_profiling", self._h)

@@ -75,7 +75,7 @@ def _paper_cases(tables, max_n):
 def _paper_check(ctx, hb, d, dp, n, kname, want):
     mode = hb.GRID_CLOSED if dp is None else hb.GRID_INTERIOR
     r = ctx.rank(hb.make_kernel(kname), hb.make_pair(d, dp, n, mode, 0), [1e-12])[0]
-    assert r.rank_lo == r.rank_hi
+    assert r.certificate in (1, 2) and r.rank_lo == r.rank_hi
     return r
 
 
@@ -122,7 +122,7 @@ def test_baseline_configs_match_oracle(ctx, hb, baseline_ranks):
                 (ties if rec["gaps"][t] < 1e-7 else mism).append(
                     (rec["d"], rec["dprime"], rec["kernel"], rec["N"], rec["tols"][t], want, r.rank,
                      rec["gaps"][t], r.gap))
-            assert r.rank_lo == r.rank_hi
+            assert r.certificate in (1, 2) and r.rank_lo == r.rank_hi
         assert res[0].sigma1 == pytest.approx(rec["sigma1"], rel=1e-11)
         if res[0].rank > 0:
             assert res[0].sigma_r == pytest.approx(rec["sigma_r"][0], rel=1e-6)
@@ -137,9 +137,14 @@ def test_full_size_properties(ctx, hb, d, dp, kname, n):
     pair = hb.make_pair(d, dp, n, hb.UNIFORM, seed)
     k = hb.make_kernel(kname)
     r = ctx.rank(k, pair, [1e-12, 1e-10, 1e-8])
-    assert all(x.rank_lo == x.rank_hi for x in r)                 # certified bracket
+    assert all(x.certificate in (1, 2) and x.rank_lo == x.rank_hi for x in r)  # certified
     assert r[0].rank >= r[1].rank >= r[2].rank                    # non-increasing in ε
     assert r[0].resid <= 0.05 * 1e-12 * r[0].sigma1 * 1.0001      # stopping rule held (eta 0.05)
+    # the deterministic-only stopping rule gives the same ranks
+    ctx.set_stopping(False)
+    rd = ctx.rank(k, pair, [1e-12, 1e-10, 1e-8])
+    ctx.set_stopping(True)
+    assert [x.rank for x in rd] == [x.rank for x in r] and all(x.certificate == 1 for x in rd)
     rt = ctx.rank(k, pair, [1e-12])[0]
     assert rt.rank == r[0].rank and rt.sigma1 == r[0].sigma1      # deterministic
 

@@ -14,6 +14,8 @@ SHAPES = [  # (transA, M, N, K, beta): name
     ((1, 120, 32768, 32768, 0.0), "W = V^T A2 (TN reduce, M=b)"),
     ((0, 128, 65536, 65536, 0.0), "sketch Y = Omega A (M=128)"),
     ((0, 16384, 16384, 32, 1.0), "band-reduction update (K=32)"),
+    ((1, 64, 32768, 32768, 0.0), "W = V^T A2 (TN reduce, M=b=64)"),
+    ((0, 32768, 32768, 64, 1.0), "trailing update (K=b=64)"),
 ]
 ctx = hb.Context(0)
 s = torch.cuda.ExternalStream(ctx.stream)
