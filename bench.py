@@ -37,17 +37,37 @@ FP64_PEAK_FILE = ROOT / "profiles" / "fp64_peak_r01.json"
 C_F = {"log_r": 84.0, "one_over_r": 76.0, "exp_neg_r": 69.0}
 
 
+# BASELINE.json configs, exactly as stated there ("doubling" frozen per SURVEY.md §8(d))
+CONFIGS = {
+    # configs[0]: d=1, [0,1] vs [1,2] (vertex), N=1000, log r, tol 1e-12
+    "c0": {"dims": {1: [0]}, "N": {1: [1000]}, "kernel": {1: "log_r"}, "tols": [1e-12]},
+    # configs[1]: d=2, edge / vertex / far, N in {1000..16000}, log r, tol 1e-12
+    "c1": {"dims": {2: [1, 0, None]}, "N": {2: [1000, 2000, 4000, 8000, 16000]},
+           "kernel": {2: "log_r"}, "tols": [1e-12]},
+    # configs[2]: d=3, face / edge / vertex / far, N = 1000..32768 doubling, 1/r, tol 1e-12
+    "c2": {"dims": {3: [2, 1, 0, None]}, "N": {3: [1000, 2000, 4000, 8000, 16000, 32768]},
+           "kernel": {3: "one_over_r"}, "tols": [1e-12]},
+    # configs[3]: d=4, d' = 0..3 + far, N = 2000..65536 doubling, exp(-r), tol 1e-10 and 1e-12
+    "c3": {"dims": {4: [0, 1, 2, 3, None]}, "N": {4: [2000, 4000, 8000, 16000, 32000, 65536]},
+           "kernel": {4: "exp_neg_r"}, "tols": [1e-12, 1e-10]},
+}
+
+
 def workload(name: str):
+    """List of (d, d', kernel, N, tols).  "sweep" = configs[4] (294 problems)."""
     probs = []
-    dims = {"sweep": [1, 2, 3, 4], "d1": [1], "d2": [2], "d3": [3], "d4": [4]}[name]
-    for n in NS:
-        for d in dims:
-            for dp in list(range(d)) + [None]:
-                for k in KERNELS:
-                    if name != "sweep":  # per-config kernel sets of BASELINE.json configs[0..3]
-                        if k != {1: "log_r", 2: "log_r", 3: "one_over_r", 4: "exp_neg_r"}[d]:
-                            continue
-                    probs.append((d, dp, k, n, [1e-12, 1e-10] if d == 4 else [1e-12]))
+    if name == "sweep":
+        for n in NS:
+            for d in (1, 2, 3, 4):
+                for dp in list(range(d)) + [None]:
+                    for k in KERNELS:
+                        probs.append((d, dp, k, n, [1e-12, 1e-10] if d == 4 else [1e-12]))
+        return probs
+    cfg = CONFIGS[name]
+    for d, dps in cfg["dims"].items():
+        for n in cfg["N"][d]:
+            for dp in dps:
+                probs.append((d, dp, cfg["kernel"][d], n, list(cfg["tols"])))
     return probs
 
 
@@ -159,9 +179,11 @@ def main():
     ap.add_argument("--steps", type=int, default=1)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="sweep", choices=["sweep", "d1", "d2", "d3", "d4"])
+    ap.add_argument("--workload", default="c1", choices=["c0", "c1", "c2", "c3", "sweep"],
+                    help="BASELINE.json configs[0..3] (c0..c3) or the full configs[4] sweep")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-sample-n", type=int, default=1000)
+    ap.add_argument("--cpu-sample-max-n", type=int, default=2000,
+                    help="CPU baseline sample: the workload's problems with N <= this")
     ap.add_argument("--details", default="", help="write per-problem results/stats JSON here")
     args = ap.parse_args()
 
@@ -170,14 +192,20 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     wl = workload(args.workload)
     threads = os.cpu_count() or 1
-    cfg = {"workload": f"{args.workload}: BASELINE.json configs[4] full sweep" if args.workload == "sweep"
-           else args.workload, "problems": len(wl), "N": NS, "kernels": KERNELS,
+    names = {"c0": "BASELINE.json configs[0] (d=1 vertex, log r, N=1000)",
+             "c1": "BASELINE.json configs[1] (d=2 edge/vertex/far, log r, N=1000..16000)",
+             "c2": "BASELINE.json configs[2] (d=3 face/edge/vertex/far, 1/r, N=1000..32768)",
+             "c3": "BASELINE.json configs[3] (d=4 d'=0..3/far, exp(-r), N=2000..65536, 2 tols)",
+             "sweep": "BASELINE.json configs[4] full sweep (294 problems)"}
+    cfg = {"workload": names[args.workload], "problems": len(wl),
+           "N": sorted({w[3] for w in wl}), "kernels": sorted({w[2] for w in wl}),
            "points": "iid uniform fp64 per cube, seed = hb_problem_seed(0, d, d', N)",
-           "tol": "1e-12 (d=4: 1e-12 and 1e-10)", "entries_per_step": sum(n * n for (_, _, _, n, _) in wl),
+           "tol": sorted({t for w in wl for t in w[4]}),
+           "entries_per_step": sum(n * n for (_, _, _, n, _) in wl),
            "l2": "inputs larger than L2: every step regenerates points and re-assembles K (sum 8N^2 = "
                  f"{8 * sum(n * n for (_, _, _, n, _) in wl) / 1e12:.2f} TB written per step)",
            "parallelism": f"lpt-partition x{world}"}
-    sample = [w for w in wl if w[3] == args.cpu_sample_n]
+    sample = [w for w in wl if w[3] <= args.cpu_sample_max_n]
 
     if args.impl == "reference":
         # the reference's CPU path for this workload = the oracle port (the reference ships no
@@ -199,8 +227,8 @@ def main():
                 "config": cfg,
                 "cpu_baseline": {"value": round(v, 6), "unit": "G entries/s", "cores": threads,
                                  "kind": "port",
-                                 "sample": f"{len(sample)} sweep problems at N={args.cpu_sample_n} "
-                                           "(oracle C assembly + numpy/LAPACK gesdd)"},
+                                 "sample": f"{len(sample)} workload problems with N <= "
+                                           f"{args.cpu_sample_max_n} (oracle C assembly + numpy/LAPACK gesdd)"},
                 "e2e": {"value": round(v, 6), "unit": "G entries/s", "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)
@@ -317,9 +345,9 @@ def main():
         v, dt, ent = cpu_baseline_run(sample, threads)
         line["cpu_baseline"] = {"value": round(v, 6), "unit": "G entries/s", "cores": threads,
                                 "kind": "port",
-                                "sample": f"{len(sample)} sweep problems at N={args.cpu_sample_n} "
-                                          f"({dt:.1f} s; oracle C assembly on {threads} threads + "
-                                          "numpy/LAPACK gesdd)"}
+                                "sample": f"{len(sample)} workload problems with N <= "
+                                          f"{args.cpu_sample_max_n} ({dt:.1f} s; oracle C assembly on "
+                                          f"{threads} threads + numpy/LAPACK gesdd)"}
     if args.details:
         Path(args.details).write_text(json.dumps({
             "results": [[r.__dict__ for r in res] for res in full], "workload": wl,

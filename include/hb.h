@@ -130,8 +130,9 @@ void hb_context_destroy(hb_context* ctx);
 void* hb_context_stream(hb_context* ctx);
 /* Tuning: block size cap (8..120, multiple of 8) and stop factor η (0 < η <= 0.1). */
 hb_status hb_context_set_tuning(hb_context* ctx, int32_t block_max, double eta);
-/* Stopping rule: 0 = deterministic only (stop when ‖A22‖_F <= η·tol·σ̂₁); 1 (default) = also
- * stop when a block power estimate gives 2·σ̂(A22) <= η·tol·σ̂₁ (probabilistic certificate). */
+/* Stopping rule: 0 (default) = deterministic only (stop when ‖A22‖_F <= η·tol·σ̂₁); 1 = also
+ * stop when a block power estimate gives 2·σ̂(A22) <= η·tol·σ̂₁ (probabilistic certificate);
+ * default 0: the residual checks cost more than the columns they save on the BASELINE sweep. */
 hb_status hb_context_set_stopping(hb_context* ctx, int32_t spectral);
 
 /* k1: seeded / grid points, SoA (coordinate k of point i at k*n + i), device pointers. */
@@ -170,7 +171,8 @@ hb_status hb_sweep(const hb_problem* probs, int64_t n, const int32_t* devices, i
 enum {
   HB_PH_ASSEMBLY = 0, HB_PH_SKETCH = 1, HB_PH_PIVOT = 2, HB_PH_PANEL = 3, HB_PH_UPDATE = 4,
   HB_PH_DOWNDATE = 5, HB_PH_SIGMA1 = 6, HB_PH_CERT_QR = 7, HB_PH_BIDIAG = 8, HB_PH_BISECT = 9,
-  HB_NPHASE = 10
+  HB_PH_CHASE = 10, /* bulge-chasing share of HB_PH_BIDIAG (stage 2) */
+  HB_NPHASE = 11
 };
 typedef struct {
   double phase_ms[HB_NPHASE];

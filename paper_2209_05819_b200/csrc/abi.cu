@@ -257,7 +257,8 @@ void hb_context_destroy(hb_context* ctx) {
 
 const char* hb_phase_name(int32_t ph) {
   static const char* names[HB_NPHASE] = {"assembly", "sketch", "pivot", "panel", "update",
-                                         "downdate", "sigma1", "cert_qr", "bidiag", "bisect"};
+                                         "downdate", "sigma1", "cert_qr", "bidiag", "bisect",
+                                         "chase"};
   return (ph >= 0 && ph < HB_NPHASE) ? names[ph] : "?";
 }
 
@@ -455,6 +456,9 @@ void hb_sweep_release(void) {
   for (auto* c : cs) hb_context_destroy(c);
 }
 
+static constexpr int64_t kSmallN = 8192;  // problems up to this N share the GPU ...
+static constexpr int kSubStreams = 4;      // ... on this many concurrent streams
+
 hb_status hb_sweep_ex(const hb_problem* probs, int64_t n, const int32_t* devices, int32_t ndev,
                       hb_rank_result* out, int32_t* status_out, hb_sweep_opts* opts) {
   if (n < 0 || (n > 0 && (!probs || !out)) || ndev < 1 || ndev > HB_MAX_DEVICES || !devices)
@@ -488,11 +492,53 @@ hb_status hb_sweep_ex(const hb_problem* probs, int64_t n, const int32_t* devices
     std::stable_sort(mine.begin(), mine.end(), [&](int64_t a, int64_t b) { return cost[a] > cost[b]; });
     cudaSetDevice(c->device);
     cudaEventRecord(c->ev[5], c->stream);
+    // Large problems (N > kSmallN) one at a time with the whole GPU; then the small ones on
+    // kSubStreams concurrent streams, each capped to 1/kSubStreams of the SMs for its
+    // cooperative grids (their sum always fits, so co-resident barriers cannot deadlock).
+    std::vector<int64_t> small;
     for (int64_t i : mine) {
       const hb_problem& p = probs[i];
+      if (std::max(p.pair.n_target, p.pair.n_source) <= kSmallN) {
+        small.push_back(i);
+        continue;
+      }
       st[i] = hb_rank(c, &p.kernel, &p.pair, p.tols, p.ntol, out + offset[i]);
     }
-    // device span of this worker: first event to last completion on its stream
+    std::vector<hb_context*> subs;
+    if (!small.empty()) {
+      std::atomic<size_t> next{0};
+      cudaEvent_t ready;
+      cudaEventCreateWithFlags(&ready, cudaEventDisableTiming);
+      cudaEventRecord(ready, c->stream);
+      const int nsub = (int)std::min<size_t>(kSubStreams, small.size());
+      std::vector<std::thread> sth;
+      std::mutex sub_mu;
+      auto sub_worker = [&](int s) {
+        hb_status ss = HB_OK;
+        hb_context* sc = cached_context(devices[w], 1000 + slot[w] * 16 + s, &ss);
+        if (!sc) {
+          for (size_t q = next.fetch_add(1); q < small.size(); q = next.fetch_add(1)) st[small[q]] = ss;
+          return;
+        }
+        {
+          std::lock_guard<std::mutex> lk(sub_mu);
+          subs.push_back(sc);
+        }
+        sc->coop_sms = std::max(1, c->num_sms / nsub);
+        sc->profiling = c->profiling;
+        cudaStreamWaitEvent(sc->stream, ready, 0);
+        for (size_t q = next.fetch_add(1); q < small.size(); q = next.fetch_add(1)) {
+          const hb_problem& p = probs[small[q]];
+          st[small[q]] = hb_rank(sc, &p.kernel, &p.pair, p.tols, p.ntol, out + offset[small[q]]);
+        }
+        cudaEventRecord(sc->ev[5], sc->stream);
+      };
+      for (int s = 0; s < nsub; ++s) sth.emplace_back(sub_worker, s);
+      for (auto& t : sth) t.join();
+      for (auto* sc : subs) cudaStreamWaitEvent(c->stream, sc->ev[5], 0);
+      cudaEventDestroy(ready);
+    }
+    // device span of this worker: first event to last completion on its streams
     cudaEvent_t end;
     cudaEventCreate(&end);
     cudaEventRecord(end, c->stream);

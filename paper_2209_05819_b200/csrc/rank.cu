@@ -81,7 +81,7 @@ void panel_and_T(hb_context* c, double* P, int64_t ld, int64_t mp, int b, double
   cudaStream_t st = c->stream;
   double* slots = ws<double>(c, B_SLOTS, (size_t)c->num_sms * (kBlockMax + 1) * 2 + 64);
   double* scal2 = ws<double>(c, B_PSCAL, 8);
-  const int G = clampi(ceil_div(mp, 64), 1, c->num_sms);
+  const int G = clampi(ceil_div(mp, 64), 1, c->coop_sms);
   const int64_t chunk = ceil_div(mp, G);
   const int64_t budget = (200 * 1024) / 8;  // doubles of shared memory per CTA
   int bsub = (int)std::min<int64_t>(b, budget / (chunk + 2) - 1);
@@ -90,7 +90,7 @@ void panel_and_T(hb_context* c, double* P, int64_t ld, int64_t mp, int b, double
     // very tall panel: global-memory fallback kernel
     PanelParams pp{};
     pp.P = P; pp.ld = ld; pp.mp = mp; pp.b = b;
-    const int Gf = clampi(ceil_div(mp, 256), 1, c->num_sms);
+    const int Gf = clampi(ceil_div(mp, 256), 1, c->coop_sms);
     pp.chunk = ceil_div(mp, Gf);
     pp.tau = tau; pp.V = V; pp.ldv = ldv;
     pp.nslot = slots; pp.wslot = slots + c->num_sms;
@@ -113,7 +113,7 @@ void panel_and_T(hb_context* c, double* P, int64_t ld, int64_t mp, int b, double
     }
     PanelParams pp{};
     pp.P = P + c0 + c0 * ld; pp.ld = ld; pp.mp = mps; pp.b = bs;
-    const int Gs = clampi(ceil_div(mps, 64), 1, c->num_sms);
+    const int Gs = clampi(ceil_div(mps, 64), 1, c->coop_sms);
     pp.chunk = ceil_div(mps, Gs);
     pp.tau = tau + c0; pp.V = V + c0 + c0 * ldv; pp.ldv = ldv;
     pp.nslot = slots; pp.wslot = slots + c->num_sms; pp.scal = scal2;
@@ -172,7 +172,7 @@ double sigma_max_rows(hb_context* c, const double* R, int64_t ld, int rows, int6
   pw.R = R; pw.ld = ld; pw.b = rows; pw.n = n; pw.iters = iters; pw.mask = 0; pw.yout = yout;
   pw.slots = ws<double>(c, B_SIG1, (size_t)2 * c->num_sms * (kBlockMax + 1));
   pw.out = out + 8; pw.bar = barrier(c);
-  coop(power_sigma1_kernel, clampi(ceil_div(n, 256), 1, c->num_sms), 0, c->stream, pw);
+  coop(power_sigma1_kernel, clampi(ceil_div(n, 256), 1, c->coop_sms), 0, c->stream, pw);
   double h = 0.0;
   sync_to_host(c, out + 8, &h, sizeof(double));
   return h;
@@ -297,6 +297,7 @@ void two_stage_bidiag(hb_context* c, double* Mk, int64_t ldm, int64_t k, double*
     gemm(g3);
   }
   // stage 2: band -> bidiagonal
+  Phase ph_chase(c, HB_PH_CHASE);
   const int W = 3 * kBand + 1;
   double* Bd = ws<double>(c, B_CERT_B2, (size_t)k * W);
   band_extract_kernel<<<(unsigned)ceil_div(k * W, 256), 256, 0, st>>>(Mk, ldm, k, kBand, Bd);
@@ -306,7 +307,7 @@ void two_stage_bidiag(hb_context* c, double* Mk, int64_t ldm, int64_t k, double*
     HB_CUDA(cudaMemsetAsync(prog, 0, sizeof(int) * k, st));
     int per_sm = 0;
     HB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bulge_chase_kernel, 128, 0));
-    const int G = clampi(k - 1, 1, std::max(1, std::min(per_sm, 8)) * c->num_sms);
+    const int G = clampi(k - 1, 1, std::max(1, std::min(per_sm, 8)) * c->coop_sms);
     int kb = kBand;
     int64_t kk = k;
     void* args[] = {&Bd, &kk, &kb, &prog};
@@ -382,7 +383,7 @@ void rank_matrix_inplace(hb_context* c, double* A, int64_t m, int64_t n, int64_t
       sp.out_b = beff; sp.bar = barrier(c);
       {
         Phase ph(c, HB_PH_PIVOT);
-        const int Gs = clampi(ceil_div(n_tr, 64), 1, 2 * c->num_sms);
+        const int Gs = clampi(ceil_div(n_tr, 64), 1, 2 * c->coop_sms);
         coop(sketch_cpqr_kernel, Gs, (size_t)ceil_div(n_tr, Gs) * sizeof(double), st, sp);
       }
       int bh = 0;
@@ -429,7 +430,7 @@ void rank_matrix_inplace(hb_context* c, double* A, int64_t m, int64_t n, int64_t
         pw.R = A; pw.ld = lda; pw.b = bh; pw.n = n; pw.iters = 40; pw.mask = 1;
         pw.slots = ws<double>(c, B_SIG1, (size_t)2 * c->num_sms * (kBlockMax + 1));
         pw.out = scal + 1; pw.bar = barrier(c);
-        coop(power_sigma1_kernel, clampi(ceil_div(n, 256), 1, c->num_sms), 0, st, pw);
+        coop(power_sigma1_kernel, clampi(ceil_div(n, 256), 1, c->coop_sms), 0, st, pw);
       }
       if (n2 > 0) {
         Phase ph(c, HB_PH_DOWNDATE);
@@ -624,6 +625,7 @@ void context_init(hb_context* c, int device) {
   HB_CUDA(cudaSetDevice(device));
   HB_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
   HB_CUDA(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
+  c->coop_sms = c->num_sms;
   cudaMemPool_t pool;
   HB_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
   uint64_t thr = UINT64_MAX;

@@ -69,9 +69,9 @@ class hb_rank_result(ctypes.Structure):
                 for f, _ in self._fields_}
 
 
-NPHASE = 10
+NPHASE = 11
 PHASES = ["assembly", "sketch", "pivot", "panel", "update", "downdate", "sigma1", "cert_qr",
-          "bidiag", "bisect"]
+          "bidiag", "bisect", "chase"]
 MAX_DEVICES = 64
 
 
