@@ -337,7 +337,9 @@ def main():
         "clocks": clocks,
         "parity": {"checked_vs_oracle": checked, "equal": equal, "mismatches": mism[:20],
                    "uncertified_brackets": uncert, "probabilistic_certificates": prob_cert,
-                   "statuses_ok": all(s == 0 for s in statuses)},
+                   "statuses_ok": all(s == 0 for s in statuses),
+                   "failed": [[list(w[:4]), s] for w, s in zip([wl[i] for i in mine], statuses) if s != 0][:10],
+                   "last_error": hb.load().hb_last_error(None).decode()[:200]},
         "phase_ms": {k: round(v, 1) for k, v in stats["phase_ms"].items()},
         "gemm_ms": round(stats["gemm_ms"], 1),
     }

@@ -252,7 +252,7 @@ void sketch(hb_context* c, const double* A, int64_t lda, int64_t m, int64_t n, d
 
 // Two-stage Golub–Kahan bidiagonalisation of the k x k upper triangle Mk (destroyed):
 // stage 1 dense -> upper band (bandwidth kBand) with DMMA GEMM updates, stage 2 bulge chasing.
-constexpr int kBand = 32;
+constexpr int kBand = 64;  // band width of stage 1 (64: full DMMA tiles, half the panel steps of 32)
 
 void two_stage_bidiag(hb_context* c, double* Mk, int64_t ldm, int64_t k, double* d, double* e,
                       double* V, int64_t ldv, double* tau, double* T) {
@@ -306,12 +306,12 @@ void two_stage_bidiag(hb_context* c, double* Mk, int64_t ldm, int64_t k, double*
     int* prog = ws<int>(c, B_PROG, (size_t)k);
     HB_CUDA(cudaMemsetAsync(prog, 0, sizeof(int) * k, st));
     int per_sm = 0;
-    HB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bulge_chase_kernel, 128, 0));
+    HB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bulge_chase_kernel, 256, 0));
     const int G = clampi(k - 1, 1, std::max(1, std::min(per_sm, 8)) * c->coop_sms);
     int kb = kBand;
     int64_t kk = k;
     void* args[] = {&Bd, &kk, &kb, &prog};
-    HB_CUDA(cudaLaunchCooperativeKernel((const void*)bulge_chase_kernel, dim3(G), dim3(128), args, 0, st));
+    HB_CUDA(cudaLaunchCooperativeKernel((const void*)bulge_chase_kernel, dim3(G), dim3(256), args, 0, st));
     launch_counter().fetch_add(1);
   }
   band_bidiag_out<<<(unsigned)ceil_div(k, 256), 256, 0, st>>>(Bd, k, kBand, d, e);
@@ -540,7 +540,7 @@ void rank_matrix_inplace(hb_context* c, double* A, int64_t m, int64_t n, int64_t
       SigmaQuery* dq = ws<SigmaQuery>(c, B_QUERY, 2 * HB_MAX_TOLS);
       SigmaAnswer* da = ws<SigmaAnswer>(c, B_ANSWER, 2 * HB_MAX_TOLS);
       HB_CUDA(cudaMemcpyAsync(dq, hq, sizeof(SigmaQuery) * nq, cudaMemcpyHostToDevice, st));
-      sigma_queries_kernel<<<1, 32 * 2 * HB_MAX_TOLS, 0, st>>>(d, e, k, dq, nq, da);
+      sigma_queries_kernel<<<1, 32 * 4 * HB_MAX_TOLS, 0, st>>>(d, e, k, dq, nq, da);
       HB_LAUNCH_CHECK();
       sync_to_host(c, da, ans, sizeof(SigmaAnswer) * nq);
     }

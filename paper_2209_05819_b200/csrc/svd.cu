@@ -180,11 +180,25 @@ __device__ int64_t count_less(const double* __restrict__ d, const double* __rest
 
 // j-th largest singular value (1-based) by 32-way multisection within [lo, hi] (warp-wide).
 __device__ double kth_largest(const double* d, const double* e, int64_t k, int64_t j, double lo,
-                              double hi, double pivmin) {
+                              double hi, double pivmin, double rel = 4e-16) {
   const int lane = threadIdx.x & 31;
   const int64_t need = k - j + 1;  // σ_(j) = inf{x : count_less(x) >= need}
+  // geometric multisection while the bracket spans more than a factor 4 (σ's near the
+  // threshold can sit many decades below σ₁), then linear multisection to relative `rel`
+  if (!(lo > 0.0)) lo = hi * 1e-300;
+  for (int it = 0; it < 12 && hi > 4.0 * lo; ++it) {
+    const double lr = log(hi / lo);
+    const double x = lo * exp(lr * (double)(lane + 1) / 33.0);
+    const bool pred = count_less(d, e, k, x, pivmin) >= need;
+    const unsigned mask = __ballot_sync(0xffffffffu, pred);
+    const int first = mask ? __ffs(mask) - 1 : 32;
+    const double nlo = first == 0 ? lo : lo * exp(lr * (double)first / 33.0);
+    const double nhi = first == 32 ? hi : lo * exp(lr * (double)(first + 1) / 33.0);
+    lo = __shfl_sync(0xffffffffu, nlo, 0);
+    hi = __shfl_sync(0xffffffffu, nhi, 0);
+  }
   for (int it = 0; it < 40; ++it) {
-    if (!(hi - lo > 4e-16 * hi)) break;
+    if (!(hi - lo > rel * hi)) break;
     const double x = lo + (hi - lo) * (double)(lane + 1) / 33.0;
     const bool pred = count_less(d, e, k, x, pivmin) >= need;
     const unsigned mask = __ballot_sync(0xffffffffu, pred);
@@ -226,24 +240,28 @@ __global__ void sigma_queries_kernel(const double* __restrict__ d, const double*
   }
   __syncthreads();
   const double s1 = sh_s1, pivmin = sh_pivmin;
-  for (int qi = warp; qi < nq; qi += blockDim.x / 32) {
+  // two warps per query: one bisects σ_p, the other σ_{p+1} (both need p: one count each)
+  for (int task = warp; task < 2 * nq; task += blockDim.x / 32) {
+    const int qi = task >> 1, half = task & 1;
     const double thr = q[qi].tol * s1;
     const double xp = nextafter(thr, 1e308);
-    int64_t p = k - count_less(d, e, k, xp, pivmin);
-    const double thr2 = thr * thr - q[qi].delta * q[qi].delta;
-    const double thr_hi = thr2 > 0.0 ? sqrt(thr2) : 0.0;
-    const int64_t phi = thr_hi > 0.0 ? k - count_less(d, e, k, nextafter(thr_hi, 1e308), pivmin) : k;
-    double sp = 0.0, sp1 = 0.0;
-    if (!q[qi].counts_only) {
-      if (p >= 1) sp = kth_largest(d, e, k, p, thr, sh_ub, pivmin);
-      if (p + 1 <= k) sp1 = kth_largest(d, e, k, p + 1, 0.0, xp, pivmin);
-    }
-    if (lane == 0) {
-      out[qi].sigma1 = s1;
-      out[qi].sigma_p = sp;
-      out[qi].sigma_p1 = sp1;
-      out[qi].rank_lo = (int)p;
-      out[qi].rank_hi = (int)phi;
+    const int64_t p = k - count_less(d, e, k, xp, pivmin);
+    if (half == 0) {
+      const double thr2 = thr * thr - q[qi].delta * q[qi].delta;
+      const double thr_hi = thr2 > 0.0 ? sqrt(thr2) : 0.0;
+      const int64_t phi = thr_hi > 0.0 ? k - count_less(d, e, k, nextafter(thr_hi, 1e308), pivmin) : k;
+      double sp = 0.0;
+      if (!q[qi].counts_only && p >= 1) sp = kth_largest(d, e, k, p, thr, sh_ub, pivmin, 1e-13);
+      if (lane == 0) {
+        out[qi].sigma1 = s1;
+        out[qi].sigma_p = sp;
+        out[qi].rank_lo = (int)p;
+        out[qi].rank_hi = (int)phi;
+      }
+    } else {
+      double sp1 = 0.0;
+      if (!q[qi].counts_only && p + 1 <= k) sp1 = kth_largest(d, e, k, p + 1, 0.0, xp, pivmin, 1e-13);
+      if (lane == 0) out[qi].sigma_p1 = sp1;
     }
   }
 }
@@ -335,7 +353,7 @@ __device__ bool chase_task(int64_t s, int t, int64_t k, int nb, ChaseTask* tk) {
     tk->right = true;
     tk->idx = q == 0 ? s : s + 1 + (int64_t)(q - 1) * nb;
     tk->lo = c0; tk->hi = c1;
-    tk->alo = tk->idx; tk->ahi = min(k - 1, c1 + nb - 1);
+    tk->alo = tk->idx; tk->ahi = min(min(k - 1, c1 + nb - 1), tk->idx + 2 * (int64_t)nb - 1);
     return true;
   }
   if (!(c1 > c0)) return false;
@@ -361,14 +379,15 @@ __device__ __forceinline__ bool band_in(int64_t r, int64_t c, int nb) {
   return o >= -nb && o <= 2 * nb;
 }
 
-__global__ void __launch_bounds__(128) bulge_chase_kernel(double* __restrict__ Bd, int64_t k, int nb,
+// One CTA (8 warps) per sweep slot; reflectors up to 64 long (nb <= 64).
+__global__ void __launch_bounds__(256) bulge_chase_kernel(double* __restrict__ Bd, int64_t k, int nb,
                                                           int* __restrict__ prog) {
   const int W = 3 * nb + 1;
   const int G = gridDim.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  constexpr int NW = 4;
-  __shared__ double v[32];
-  __shared__ double wv[96];
+  constexpr int NW = 8;
+  __shared__ double v[64];
+  __shared__ double wpart[2][128];
   __shared__ double sh[4];
   volatile int* vprog = prog;
   for (int64_t s = blockIdx.x; s < k - 1; s += G) {
@@ -384,16 +403,21 @@ __global__ void __launch_bounds__(128) bulge_chase_kernel(double* __restrict__ B
         __threadfence();
       }
       const int len = (int)(tk.hi - tk.lo + 1);
-      // reflector from the segment (warp 0)
+      // reflector from the segment (warp 0, two elements per lane)
       if (warp == 0) {
-        double x = 0.0;
-        if (lane < len) {
-          const int64_t r = tk.right ? tk.idx : tk.lo + lane;
-          const int64_t c = tk.right ? tk.lo + lane : tk.idx;
-          x = __ldcg(Bd + band_off(r, c, nb, W));
+        double x[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int el = lane + 32 * h;
+          x[h] = 0.0;
+          if (el < len) {
+            const int64_t r = tk.right ? tk.idx : tk.lo + el;
+            const int64_t c = tk.right ? tk.lo + el : tk.idx;
+            x[h] = __ldcg(Bd + band_off(r, c, nb, W));
+          }
         }
-        const double alpha = __shfl_sync(0xffffffffu, x, 0);
-        double ss = lane > 0 ? x * x : 0.0;
+        const double alpha = __shfl_sync(0xffffffffu, x[0], 0);
+        double ss = (lane > 0 ? x[0] * x[0] : 0.0) + x[1] * x[1];
         ss = warp_sum(ss);
         double tau = 0.0, scal = 0.0, beta = alpha;
         if (ss > 0.0) {
@@ -401,28 +425,30 @@ __global__ void __launch_bounds__(128) bulge_chase_kernel(double* __restrict__ B
           tau = (beta - alpha) / beta;
           scal = 1.0 / (alpha - beta);
         }
-        v[lane] = lane == 0 ? 1.0 : (lane < len ? x * scal : 0.0);
+        v[lane] = lane == 0 ? 1.0 : (lane < len ? x[0] * scal : 0.0);
+        v[lane + 32] = lane + 32 < len ? x[1] * scal : 0.0;
         if (lane == 0) { sh[0] = tau; sh[1] = beta; }
       }
       __syncthreads();
       const double tau = sh[0];
       if (tau != 0.0) {
         if (tk.right) {
-          // rows r in [alo, ahi]: s_r = sum_c M[r, lo + c] v_c ; M[r, .] -= tau s_r v.
-          // A warp owns up to 16 rows; all their loads are issued before the reductions.
+          // rows r in [alo, ahi] (<= 127): s_r = sum_c M[r, lo + c] v_c; M[r, .] -= tau s_r v.
+          // A warp owns up to 16 rows; all loads are issued before the reductions.
           constexpr int RMAX = 16;
-          const int64_t c = tk.lo + lane;
-          const double vl = v[lane];
-          double mv[RMAX];
+          const double v0 = v[lane], v1 = v[lane + 32];
+          double m0[RMAX], m1[RMAX], sr[RMAX];
 #pragma unroll
           for (int j = 0; j < RMAX; ++j) {
             const int64_t r = tk.alo + warp + (int64_t)j * NW;
-            const bool ok = r <= tk.ahi && lane < len && band_in(r, c, nb);
-            mv[j] = ok ? __ldcg(Bd + band_off(r, c, nb, W)) : 0.0;
+            const int64_t c0 = tk.lo + lane, c1 = c0 + 32;
+            const bool ok0 = r <= tk.ahi && lane < len && band_in(r, c0, nb);
+            const bool ok1 = r <= tk.ahi && lane + 32 < len && band_in(r, c1, nb);
+            m0[j] = ok0 ? __ldcg(Bd + band_off(r, c0, nb, W)) : 0.0;
+            m1[j] = ok1 ? __ldcg(Bd + band_off(r, c1, nb, W)) : 0.0;
           }
-          double sr[RMAX];
 #pragma unroll
-          for (int j = 0; j < RMAX; ++j) sr[j] = mv[j] * vl;
+          for (int j = 0; j < RMAX; ++j) sr[j] = m0[j] * v0 + m1[j] * v1;
 #pragma unroll
           for (int o = 16; o > 0; o >>= 1)
 #pragma unroll
@@ -430,39 +456,55 @@ __global__ void __launch_bounds__(128) bulge_chase_kernel(double* __restrict__ B
 #pragma unroll
           for (int j = 0; j < RMAX; ++j) {
             const int64_t r = tk.alo + warp + (int64_t)j * NW;
-            const bool ok = r <= tk.ahi && lane < len && band_in(r, c, nb);
-            if (ok) __stcg(Bd + band_off(r, c, nb, W), mv[j] - tau * sr[j] * vl);
+            const int64_t c0 = tk.lo + lane, c1 = c0 + 32;
+            if (r <= tk.ahi && lane < len && band_in(r, c0, nb))
+              __stcg(Bd + band_off(r, c0, nb, W), m0[j] - tau * sr[j] * v0);
+            if (r <= tk.ahi && lane + 32 < len && band_in(r, c1, nb))
+              __stcg(Bd + band_off(r, c1, nb, W), m1[j] - tau * sr[j] * v1);
           }
         } else {
-          // columns c in [alo, ahi] (one per thread): w_c = sum_r v_r M[lo + r, c];
-          // M[., c] -= tau v w_c.  The column segment is held in registers.
+          // columns c in [alo, ahi] (<= 128): thread (cc, half) holds 32 rows of column cc;
+          // w_c = sum_r v_r M[lo + r, c] combined over the two halves; M[., c] -= tau v w_c.
           const int ncols = (int)(tk.ahi - tk.alo + 1);
-          for (int cc = tid; cc < ncols; cc += 128) {
-            const int64_t c = tk.alo + cc;
-            double x[32];
+          const int cc = tid & 127, half = tid >> 7;
+          const int64_t c = tk.alo + cc;
+          double x[32];
+          double w = 0.0;
+          if (cc < ncols) {
 #pragma unroll
             for (int r = 0; r < 32; ++r) {
-              const bool ok = r < len && band_in(tk.lo + r, c, nb);
-              x[r] = ok ? __ldcg(Bd + band_off(tk.lo + r, c, nb, W)) : 0.0;
+              const int rr = half * 32 + r;
+              const bool ok = rr < len && band_in(tk.lo + rr, c, nb);
+              x[r] = ok ? __ldcg(Bd + band_off(tk.lo + rr, c, nb, W)) : 0.0;
             }
-            double w = 0.0;
 #pragma unroll
-            for (int r = 0; r < 32; ++r) w += v[r] * x[r];
-            w *= tau;
+            for (int r = 0; r < 32; ++r) w += v[half * 32 + r] * x[r];
+            wpart[half][cc] = w;
+          }
+          __syncthreads();
+          if (cc < ncols) {
+            w = (wpart[0][cc] + wpart[1][cc]) * tau;
 #pragma unroll
             for (int r = 0; r < 32; ++r) {
-              const bool ok = r < len && band_in(tk.lo + r, c, nb);
-              if (ok) __stcg(Bd + band_off(tk.lo + r, c, nb, W), x[r] - v[r] * w);
+              const int rr = half * 32 + r;
+              if (rr < len && band_in(tk.lo + rr, c, nb))
+                __stcg(Bd + band_off(tk.lo + rr, c, nb, W), x[r] - v[rr] * w);
             }
           }
         }
       }
       __syncthreads();
       // exact zeros / beta on the annihilated segment
-      if (warp == 0 && lane < len) {
-        const int64_t r = tk.right ? tk.idx : tk.lo + lane;
-        const int64_t c = tk.right ? tk.lo + lane : tk.idx;
-        __stcg(Bd + band_off(r, c, nb, W), lane == 0 ? sh[1] : 0.0);
+      if (warp == 0) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int el = lane + 32 * h;
+          if (el < len) {
+            const int64_t r = tk.right ? tk.idx : tk.lo + el;
+            const int64_t c = tk.right ? tk.lo + el : tk.idx;
+            __stcg(Bd + band_off(r, c, nb, W), el == 0 ? sh[1] : 0.0);
+          }
+        }
       }
       __syncthreads();
       if (tid == 0) {

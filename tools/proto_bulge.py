@@ -51,7 +51,7 @@ def tasks_of_sweep(s, k, nb):
         c1 = min(c0 + nb - 1, k - 1)
         row = s if q == 0 else s + 1 + (q - 1) * nb
         if c1 > c0 or q == 0:
-            out.append(("R", row, c0, c1, row, min(k - 1, c1 + nb - 1)))
+            out.append(("R", row, c0, c1, row, min(k - 1, c1 + nb - 1, row + 2 * nb - 1)))
         # left step: rows [c0, c1], annihilate column c0 below row c0
         if c1 > c0:
             out.append(("L", c0, c0, c1, c0, min(k - 1, c1 + nb)))
