@@ -126,6 +126,13 @@ void rank_pair(hb_context* c, const hb_kernel* kernel, const hb_pair* pair, cons
   check_pair(pair);
   check_tols(tols, ntol);
   HB_CUDA(cudaSetDevice(c->device));
+  {
+    // a non-sticky error left by an earlier unchecked runtime call on this host thread must not
+    // be reported as this problem's launch failure (sticky device faults still surface at sync)
+    const cudaError_t stale = cudaGetLastError();
+    if (stale != cudaSuccess && getenv("HB_DEBUG"))
+      fprintf(stderr, "[hb] cleared stale CUDA error before problem: %s\n", cudaGetErrorString(stale));
+  }
   const int d = pair->target.d;
   const int64_t m = pair->n_target, n = pair->n_source;
   const int64_t lda = hb::round_up(m, 8);
@@ -456,7 +463,8 @@ void hb_sweep_release(void) {
   for (auto* c : cs) hb_context_destroy(c);
 }
 
-static constexpr int64_t kSmallN = 8192;  // problems up to this N share the GPU ...
+static constexpr int64_t kSmallN = 16384;   // problems up to this N ...
+static constexpr double kSmallRank = 1000.0; // ... and this predicted rank share the GPU ...
 static constexpr int kSubStreams = 4;      // ... on this many concurrent streams
 
 hb_status hb_sweep_ex(const hb_problem* probs, int64_t n, const int32_t* devices, int32_t ndev,
@@ -492,13 +500,15 @@ hb_status hb_sweep_ex(const hb_problem* probs, int64_t n, const int32_t* devices
     std::stable_sort(mine.begin(), mine.end(), [&](int64_t a, int64_t b) { return cost[a] > cost[b]; });
     cudaSetDevice(c->device);
     cudaEventRecord(c->ev[5], c->stream);
-    // Large problems (N > kSmallN) one at a time with the whole GPU; then the small ones on
+    // Large problems one at a time with the whole GPU; then the small ones (N <= kSmallN and
+    // predicted rank <= kSmallRank: latency-bound, few blocks) on
     // kSubStreams concurrent streams, each capped to 1/kSubStreams of the SMs for its
     // cooperative grids (their sum always fits, so co-resident barriers cannot deadlock).
     std::vector<int64_t> small;
     for (int64_t i : mine) {
       const hb_problem& p = probs[i];
-      if (std::max(p.pair.n_target, p.pair.n_source) <= kSmallN) {
+      const int64_t np = std::max(p.pair.n_target, p.pair.n_source);
+      if (np <= kSmallN && predicted_rank(p.pair.target.d, p.pair.d_prime, np) <= kSmallRank) {
         small.push_back(i);
         continue;
       }

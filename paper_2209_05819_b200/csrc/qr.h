@@ -99,6 +99,8 @@ __global__ void write_lower_from_R(const double* R, int64_t ldr, int b, int nc, 
 __global__ void band_extract_kernel(const double* M, int64_t ldm, int64_t k, int nb, double* Bd);
 __global__ void band_bidiag_out(const double* Bd, int64_t k, int nb, double* d, double* e);
 __global__ void bulge_chase_kernel(double* Bd, int64_t k, int nb, int* prog);
+__global__ void bidiag_small_kernel(const double* Mk, int64_t ldm, int k, double* d, double* e);
+constexpr int kSmallBidiag = 144;  // k x k triangle up to this size: one-CTA shared-memory bidiag
 __global__ void sigma_queries_kernel(const double* d, const double* e, int64_t k,
                                      const SigmaQuery* q, int nq, SigmaAnswer* out);
 __global__ void sigma_all_kernel(const double* d, const double* e, int64_t k, double sigma_max,

@@ -257,6 +257,14 @@ constexpr int kBand = 64;  // band width of stage 1 (64: full DMMA tiles, half t
 void two_stage_bidiag(hb_context* c, double* Mk, int64_t ldm, int64_t k, double* d, double* e,
                       double* V, int64_t ldv, double* tau, double* T) {
   cudaStream_t st = c->stream;
+  if (k <= kSmallBidiag) {  // one CTA, whole triangle in shared memory
+    const size_t smem = ((size_t)k * (k + 1) + 3 * (size_t)k) * sizeof(double);
+    HB_CUDA(cudaFuncSetAttribute((const void*)bidiag_small_kernel,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    bidiag_small_kernel<<<1, 256, smem, st>>>(Mk, ldm, (int)k, d, e);
+    HB_LAUNCH_CHECK();
+    return;
+  }
   const int64_t ldp = round_up(k, 8);
   double* P2 = ws<double>(c, B_ST1_P, (size_t)ldp * kBand);
   double* X = ws<double>(c, B_ST1_X, (size_t)ldp * kBand);
@@ -427,7 +435,7 @@ void rank_matrix_inplace(hb_context* c, double* A, int64_t m, int64_t n, int64_t
       if (first) {
         Phase ph(c, HB_PH_SIGMA1);
         PowerParams pw{};
-        pw.R = A; pw.ld = lda; pw.b = bh; pw.n = n; pw.iters = 40; pw.mask = 1;
+        pw.R = A; pw.ld = lda; pw.b = bh; pw.n = n; pw.iters = 12; pw.mask = 1;  // a lower bound suffices
         pw.slots = ws<double>(c, B_SIG1, (size_t)2 * c->num_sms * (kBlockMax + 1));
         pw.out = scal + 1; pw.bar = barrier(c);
         coop(power_sigma1_kernel, clampi(ceil_div(n, 256), 1, c->coop_sms), 0, st, pw);
@@ -607,7 +615,12 @@ void prof_resolve(hb_context* c) {
   if (!c->profiling && c->marks.empty()) return;
   for (const auto& mk : c->marks) {
     float ms = 0.f;
-    if (cudaEventElapsedTime(&ms, c->evpool[mk.e0], c->evpool[mk.e1]) != cudaSuccess) continue;
+    if (mk.e0 >= c->evused || mk.e1 >= c->evused) continue;
+    cudaEventSynchronize(c->evpool[mk.e1]);
+    if (cudaEventElapsedTime(&ms, c->evpool[mk.e0], c->evpool[mk.e1]) != cudaSuccess) {
+      (void)cudaGetLastError();  // a profiling hiccup must not poison the next launch check
+      continue;
+    }
     if (mk.phase == PH_GEMM) {
       c->stats.gemm_ms += ms;
       c->stats.gemm_flops += mk.flops;

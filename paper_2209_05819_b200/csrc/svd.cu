@@ -520,3 +520,86 @@ __global__ void __launch_bounds__(256) bulge_chase_kernel(double* __restrict__ B
 }
 
 }  // namespace hb
+
+namespace hb {
+// Small certification (k <= kSmallBidiag): one CTA holds the whole k x k triangle in shared
+// memory and runs the one-stage Golub–Kahan bidiagonalisation there (no grid barriers, one
+// launch).  Column-major with odd leading dimension k+1 so column sweeps (w = uᵀM) and row sweeps
+// (z = M v) are both bank-conflict free.
+__global__ void __launch_bounds__(256) bidiag_small_kernel(const double* __restrict__ Mk, int64_t ldm,
+                                                           int k, double* __restrict__ d,
+                                                           double* __restrict__ e) {
+  extern __shared__ double S[];  // [k][k+1] + u[k] + v[k] + w[k]
+  const int ld = k + 1;
+  double* u = S + (size_t)k * ld;
+  double* vv = u + k;
+  double* w = vv + k;
+  __shared__ double sh[4];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int idx = tid; idx < k * k; idx += 256) {
+    const int r = idx % k, c = idx / k;
+    S[c * ld + r] = Mk[r + (int64_t)c * ldm];
+  }
+  __syncthreads();
+  for (int i = 0; i < k; ++i) {
+    // ---- left reflector from column i (rows i..k-1) ----
+    if (warp == 0) {
+      double s = 0.0;
+      for (int r = i + 1 + lane; r < k; r += 32) s += S[i * ld + r] * S[i * ld + r];
+      s = warp_sum(s);
+      const double alpha = S[i * ld + i];
+      double tau = 0.0, scal = 0.0, beta = alpha;
+      if (s > 0.0) {
+        beta = -copysign(sqrt(alpha * alpha + s), alpha);
+        tau = (beta - alpha) / beta;
+        scal = 1.0 / (alpha - beta);
+      }
+      for (int r = i + 1 + lane; r < k; r += 32) u[r] = S[i * ld + r] * scal;
+      if (lane == 0) { u[i] = 1.0; sh[0] = tau; d[i] = beta; }
+    }
+    __syncthreads();
+    const double tu = sh[0];
+    for (int q = i + 1 + tid; q < k; q += 256) {
+      double s = 0.0;
+      for (int r = i; r < k; ++r) s += u[r] * S[q * ld + r];
+      w[q] = s * tu;
+    }
+    __syncthreads();
+    for (int idx = tid; idx < (k - i) * (k - i - 1); idx += 256) {
+      const int r = i + idx % (k - i), q = i + 1 + idx / (k - i);
+      S[q * ld + r] -= u[r] * w[q];
+    }
+    __syncthreads();
+    if (i + 1 >= k) break;
+    // ---- right reflector from row i (columns i+1..k-1) ----
+    if (warp == 0) {
+      double s = 0.0;
+      for (int q = i + 2 + lane; q < k; q += 32) s += S[q * ld + i] * S[q * ld + i];
+      s = warp_sum(s);
+      const double alpha = S[(i + 1) * ld + i];
+      double tau = 0.0, scal = 0.0, beta = alpha;
+      if (s > 0.0) {
+        beta = -copysign(sqrt(alpha * alpha + s), alpha);
+        tau = (beta - alpha) / beta;
+        scal = 1.0 / (alpha - beta);
+      }
+      for (int q = i + 2 + lane; q < k; q += 32) vv[q] = S[q * ld + i] * scal;
+      if (lane == 0) { vv[i + 1] = 1.0; sh[1] = tau; e[i] = beta; }
+    }
+    __syncthreads();
+    const double tv = sh[1];
+    for (int r = i + 1 + tid; r < k; r += 256) {
+      double s = 0.0;
+      for (int q = i + 1; q < k; ++q) s += S[q * ld + r] * vv[q];
+      w[r] = s * tv;
+    }
+    __syncthreads();
+    for (int idx = tid; idx < (k - i - 1) * (k - i - 1); idx += 256) {
+      const int r = i + 1 + idx % (k - i - 1), q = i + 1 + idx / (k - i - 1);
+      S[q * ld + r] -= w[r] * vv[q];
+    }
+    __syncthreads();
+  }
+  if (tid == 0) e[k - 1] = 0.0;
+}
+}  // namespace hb
