@@ -2,9 +2,8 @@
 //
 // The mp x b panel is split into row chunks, one per CTA (grid-cooperative, co-resident); each
 // CTA copies its chunk into shared memory once, runs all b column steps on it, and writes R, V
-// back at the end.  Per column only two cross-CTA reductions touch global memory (the column
-// norm, and w = vᵀP for the trailing panel columns), each one grid barrier; everything else is
-// shared-memory work.  The host (rank.cu: panel_and_T) splits panels whose chunk would not fit
+// back at the end.  Per column one cross-CTA reduction touches global memory (one grid barrier,
+// below); everything else is shared-memory work.  The host (rank.cu: panel_and_T) splits panels whose chunk would not fit
 // (tall panels) into column sub-panels and joins them with DMMA GEMM updates.
 #include "common.cuh"
 #include "kernels.h"
@@ -12,107 +11,142 @@
 
 namespace hb {
 
-__global__ void __launch_bounds__(256) panel_qr_smem_kernel(PanelParams p) {
+// One grid barrier per column.  For column c every CTA publishes, over its own rows i > c, the
+// partial products g_q = Σ x_i·P[i,q] for q >= c (g_c is the squared norm below the diagonal),
+// and the CTA owning row c publishes that row.  After the barrier every CTA reduces the partials
+// itself (fixed order: deterministic, identical in all CTAs), forms the reflector
+//   β = −sign(α)·sqrt(α² + g_c),  τ = (β − α)/β,  v = (x − β e_c)/(α − β)  (v_c = 1),
+// and w_q = τ·vᵀP[:,q] = τ·(P[c,q] + g_q/(α − β)) without a second reduction, updates its rows,
+// and accumulates the partials of column c+1 in the same pass.
+__global__ void __launch_bounds__(kPanelThreads) panel_qr_smem_kernel(PanelParams p) {
+  constexpr int NW = kPanelThreads / 32;
   extern __shared__ double psm[];
+  __shared__ double red[NW][128];
+  __shared__ double sh[3];
   const int G = gridDim.x, g = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int b = p.b;
   const int64_t chunk = p.chunk;
   const int64_t r0 = g * chunk, r1 = min(p.mp, r0 + chunk);
   const int rows = (int)max((int64_t)0, r1 - r0);
-  const int ldS = (int)chunk + 1;  // odd stride: column-wise and row-wise smem access both spread
-  double* S = psm;                 // [b][ldS]
-  double* ws = psm + (size_t)b * ldS;  // [b]
-  __shared__ double sh[4];
-  __shared__ double red[32];
+  const int ldS = (int)chunk + 1;        // odd stride: column-wise and row-wise smem access both spread
+  double* S = psm;                       // [b][ldS]
+  double* ws = psm + (size_t)b * ldS;    // [b]  w_q
+  double* gs = ws + b;                   // [b]  reduced g_q
   double* P = p.P;
   const int64_t ld = p.ld;
   const int nref = (int)min((int64_t)b, p.mp);
+  double* part = p.wslot;                // [2][G][b]
+  double* rowc = p.scal;                 // [2][b]
 
-  // load the chunk (coalesced along rows)
-  for (int q = warp; q < b; q += 8)
+  for (int q = warp; q < b; q += NW)
     for (int i = lane; i < rows; i += 32) S[q * ldS + i] = P[r0 + i + (int64_t)q * ld];
   __syncthreads();
-  // column 0: partial norm over rows > 0, owner publishes alpha
-  if (warp == 0) {
-    double s = 0.0;
-    for (int i = lane; i < rows; i += 32)
-      if (r0 + i > 0) s += S[i] * S[i];
-    s = warp_sum(s);
-    if (lane == 0) {
-      p.nslot[g] = s;
-      if (r0 == 0 && rows > 0) p.scal[0] = S[0];
+  // partials of column 0
+  if (nref > 0) {
+    const int i0 = r0 == 0 ? 1 : 0;
+    for (int q = warp; q < b; q += NW) {
+      const double* Sq = S + q * ldS;
+      double s = 0.0;
+      for (int i = i0 + lane; i < rows; i += 32) s = fma(S[i], Sq[i], s);
+      s = warp_sum(s);
+      if (lane == 0) part[(size_t)g * b + q] = s;
     }
+    if (r0 == 0 && rows > 0)
+      for (int q = tid; q < b; q += kPanelThreads) rowc[q] = S[q * ldS];
   }
   grid_sync(p.bar);
 
   for (int c = 0; c < nref; ++c) {
     const int par = c & 1;
-    // ---- reflector of column c ----
+    const double* pp = part + (size_t)par * G * b;
+    const double* rc = rowc + par * b;
+    // ---- reduce the partials of column c: lanes over q, warps over CTAs, fixed order ----
     {
-      const double s = block_sum_strided(p.nslot, G, 1, red);
-      if (tid == 0) {
-        const double alpha = p.scal[par];
-        double tau = 0.0, scal = 0.0, beta = alpha;
-        if (s > 0.0) {
-          beta = -copysign(sqrt(alpha * alpha + s), alpha);
-          tau = (beta - alpha) / beta;
-          scal = 1.0 / (alpha - beta);
+      double s[4] = {0.0, 0.0, 0.0, 0.0};
+      for (int h = warp; h < G; h += NW) {
+        const double* row = pp + (size_t)h * b;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int q = c + lane + 32 * j;
+          if (q < b) s[j] += __ldcg(row + q);
         }
-        sh[0] = tau; sh[1] = scal; sh[2] = beta;
-        if (g == 0) p.tau[c] = tau;
       }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) red[warp][lane + 32 * j] = s[j];
+    }
+    __syncthreads();
+    if (tid < b - c) {
+      double t = 0.0;
+#pragma unroll
+      for (int w = 0; w < NW; ++w) t += red[w][tid];
+      gs[c + tid] = t;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      const double alpha = __ldcg(rc + c), s = gs[c];
+      double tau = 0.0, scal = 0.0, beta = alpha;
+      if (s > 0.0) {
+        beta = -copysign(sqrt(alpha * alpha + s), alpha);
+        tau = (beta - alpha) / beta;
+        scal = 1.0 / (alpha - beta);
+      }
+      sh[0] = tau; sh[1] = scal; sh[2] = beta;
+      if (g == 0) p.tau[c] = tau;
     }
     __syncthreads();
     const double tau = sh[0], scal = sh[1];
-    const int ic = (int)max((int64_t)0, (int64_t)c - r0);  // first local row >= c
+    for (int q = c + 1 + tid; q < b; q += kPanelThreads) ws[q] = tau * (__ldcg(rc + q) + scal * gs[q]);
+    const int ic = (int)max((int64_t)0, (int64_t)c - r0);        // first local row >= c
+    const int i1 = (int)max((int64_t)0, (int64_t)(c + 1) - r0);  // first local row > c
+    const int in = (int)max((int64_t)0, (int64_t)(c + 2) - r0);  // first local row > c+1
     double* Sc = S + c * ldS;
-    for (int i = ic + tid; i < rows; i += 256) {
-      if (r0 + i > c) Sc[i] *= scal;
+    for (int i = i1 + tid; i < rows; i += kPanelThreads) Sc[i] *= scal;
+    if (ic < i1 && ic < rows && tid == 0) Sc[ic] = sh[2];  // row c: R diagonal (v_c = 1 implicit)
+    __syncthreads();
+    if (c + 1 >= b) break;
+    // ---- column c+1 first (its entries feed the partials of the other columns) ----
+    {
+      double* Sq = S + (c + 1) * ldS;
+      const double wq = ws[c + 1];
+      if (ic < i1 && ic < rows && tid == 0) Sq[ic] -= wq;
+      for (int i = i1 + tid; i < rows; i += kPanelThreads) Sq[i] = fma(-Sc[i], wq, Sq[i]);
     }
     __syncthreads();
-    // v_i = Sc[i] for rows > c, 1 at row c
-    // ---- w_q = sum_i v_i P[i, q] (q > c), partial over own rows ----
-    for (int q = c + 1 + warp; q < b; q += 8) {
-      const double* Sq = S + q * ldS;
-      double s = 0.0;
-      for (int i = ic + lane; i < rows; i += 32) {
-        const double vi = (r0 + i == c) ? 1.0 : Sc[i];
-        s += vi * Sq[i];
-      }
-      s = warp_sum(s);
-      if (lane == 0) p.wslot[(size_t)g * b + q] = s;
-    }
-    grid_sync(p.bar);
-    for (int q = c + 1 + warp; q < b; q += 8) {
-      const double s = warp_sum_strided(p.wslot + q, G, b);
-      if (lane == 0) ws[q] = s * tau;
-    }
-    __syncthreads();
-    // ---- update own rows; partial norm of column c+1 (rows > c+1); owner publishes alpha ----
-    double nrm = 0.0;
-    for (int q = c + 1 + warp; q < b; q += 8) {
+    const bool more = c + 1 < nref;
+    double* pn = part + (size_t)(par ^ 1) * G * b;
+    double* rn = rowc + (par ^ 1) * b;
+    const double* Sn = S + (c + 1) * ldS;
+    const bool owner = r0 <= c + 1 && c + 1 < r1;
+    for (int q = c + 1 + warp; q < b; q += NW) {
       double* Sq = S + q * ldS;
-      const double wq = ws[q];
-      for (int i = ic + lane; i < rows; i += 32) {
-        const double vi = (r0 + i == c) ? 1.0 : Sc[i];
-        const double x = Sq[i] - vi * wq;
-        Sq[i] = x;
-        if (q == c + 1 && r0 + i > c + 1) nrm += x * x;
+      double acc = 0.0;
+      if (q > c + 1) {
+        const double wq = ws[q];
+        if (lane == 0)  // rows c and c+1 (at most two, owned by this CTA or not)
+          for (int i = ic; i < min(in, rows); ++i) Sq[i] -= (i < i1 ? 1.0 : Sc[i]) * wq;
+        for (int i = in + lane; i < rows; i += 32) {
+          const double x = fma(-Sc[i], wq, Sq[i]);
+          Sq[i] = x;
+          acc = fma(Sn[i], x, acc);
+        }
+      } else {
+        for (int i = in + lane; i < rows; i += 32) acc = fma(Sn[i], Sq[i], acc);
+      }
+      if (more) {
+        __syncwarp();
+        acc = warp_sum(acc);
+        if (lane == 0) {
+          pn[(size_t)g * b + q] = acc;
+          if (owner) rn[q] = Sq[c + 1 - r0];
+        }
       }
     }
-    if (warp == 0) {  // q == c + 1 is handled by warp 0
-      nrm = warp_sum(nrm);
-      if (lane == 0) p.nslot[g] = nrm;
-    }
-    if (r0 <= c && c < r1 && tid == 0) Sc[c - r0] = sh[2];  // R diagonal
-    __syncthreads();
-    if (c + 1 < nref && r0 <= c + 1 && c + 1 < r1 && tid == 0)
-      p.scal[par ^ 1] = S[(c + 1) * ldS + (c + 1 - r0)];
+    if (!more) break;
     grid_sync(p.bar);
   }
-  // write back R / V and the explicit V (unit diagonal, zeros above, zero columns >= nref)
-  for (int q = warp; q < b; q += 8) {
+  // the last column(s) beyond nref (wide panels) were updated in place above
+  for (int q = warp; q < b; q += NW) {
     const double* Sq = S + q * ldS;
     double* vq = p.V + (int64_t)q * p.ldv;
     double* pq = P + (int64_t)q * ld;
@@ -123,7 +157,7 @@ __global__ void __launch_bounds__(256) panel_qr_smem_kernel(PanelParams p) {
     }
   }
   if (g == 0)
-    for (int q = nref + tid; q < b; q += 256) p.tau[q] = 0.0;
+    for (int q = nref + tid; q < b; q += kPanelThreads) p.tau[q] = 0.0;
 }
 
 }  // namespace hb

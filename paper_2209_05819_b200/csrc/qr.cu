@@ -397,44 +397,56 @@ __global__ void __launch_bounds__(256) panel_qr_kernel(PanelParams p) {
     for (int q = nref + tid; q < b; q += 256) p.tau[q] = 0.0;
 }
 
-// T of the compact-WY form from S = VᵀV and τ (LAPACK dlarft, forward/columnwise).
+// T of the compact-WY form from S = VᵀV and τ (LAPACK dlarft, forward/columnwise):
+// T[0:c, c] = −τ_c · T[0:c, 0:c] · S[0:c, c].  S's strict upper triangle (packed) and T live in
+// shared memory; step c is a triangular mat-vec split over threads.
 __global__ void build_T_kernel(const double* __restrict__ S, int64_t lds, const double* __restrict__ tau,
                                int b, double* __restrict__ T, int64_t ldt) {
-  extern __shared__ double Ts[];  // b x b, ld b
+  extern __shared__ double smT[];
+  double* Ts = smT;                       // b x b, column-major, ld b
+  double* Sp = smT + (size_t)b * b;       // packed strict upper: column c at c(c-1)/2
+  __shared__ double taus[kBlockMax];
   const int t = threadIdx.x;
   for (int e = t; e < b * b; e += blockDim.x) Ts[e] = 0.0;
+  for (int c = 1; c < b; ++c)
+    for (int k = t; k < c; k += blockDim.x) Sp[c * (c - 1) / 2 + k] = S[k + (int64_t)c * lds];
+  for (int c = t; c < b; c += blockDim.x) taus[c] = tau[c];
   __syncthreads();
   for (int c = 0; c < b; ++c) {
-    const double tc = tau[c];
-    if (t < c) {
+    const double tc = taus[c];
+    const double* sc = Sp + c * (c - 1) / 2;
+    for (int r = t; r < c; r += blockDim.x) {
       double s = 0.0;
-      for (int k = t; k < c; ++k) s += Ts[t + k * b] * S[k + (int64_t)c * lds];
-      Ts[t + c * b] = -tc * s;
-    } else if (t == c) {
-      Ts[c + c * b] = tc;
+      for (int k = r; k < c; ++k) s += Ts[r + k * b] * sc[k];
+      Ts[r + c * b] = -tc * s;
     }
+    if (t == 0) Ts[c + c * b] = tc;
     __syncthreads();
   }
   for (int e = t; e < b * b; e += blockDim.x) T[(e % b) + (int64_t)(e / b) * ldt] = Ts[e];
 }
 
-// Z (ell x b) = Y1 R11^{-1}: row-wise forward substitution, one thread per sketch row.
+// Z (ell x b) = Y1 R11^{-1}: row-wise forward substitution, one thread per sketch row; R11's
+// upper triangle (packed) and Z are kept in shared memory.
 __global__ void sketch_trsm_kernel(const double* __restrict__ Y1, int64_t ldy, int ell,
                                    const double* __restrict__ R, int64_t ldr, int b,
                                    double* __restrict__ Z, int64_t ldz) {
-  extern __shared__ double Rs[];  // b x b upper
-  for (int e = threadIdx.x; e < b * b; e += blockDim.x) {
-    const int i = e % b, c = e / b;
-    Rs[e] = i <= c ? R[i + (int64_t)c * ldr] : 0.0;
-  }
+  extern __shared__ double smZ[];
+  double* Rp = smZ;                              // packed upper incl. diagonal: column c at c(c+1)/2
+  double* Zs = smZ + (size_t)b * (b + 1) / 2;    // b x ell, Zs[c * ell + t]
+  for (int c = 0; c < b; ++c)
+    for (int i = threadIdx.x; i <= c; i += blockDim.x) Rp[c * (c + 1) / 2 + i] = R[i + (int64_t)c * ldr];
   __syncthreads();
   const int t = threadIdx.x;
   if (t >= ell) return;
   for (int c = 0; c < b; ++c) {
+    const double* rc = Rp + c * (c + 1) / 2;
     double s = Y1[t + (int64_t)c * ldy];
-    for (int i = 0; i < c; ++i) s -= Z[t + (int64_t)i * ldz] * Rs[i + c * b];
-    const double d = Rs[c + c * b];
-    Z[t + (int64_t)c * ldz] = d != 0.0 ? s / d : 0.0;
+    for (int i = 0; i < c; ++i) s -= Zs[i * ell + t] * rc[i];
+    const double d = rc[c];
+    const double z = d != 0.0 ? s / d : 0.0;
+    Zs[c * ell + t] = z;
+    Z[t + (int64_t)c * ldz] = z;
   }
 }
 

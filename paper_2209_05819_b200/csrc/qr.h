@@ -24,6 +24,8 @@ struct SketchParams {
   GridBarrier bar;
 };
 
+constexpr int kPanelThreads = 512;  // panel_qr_smem_kernel block size
+
 struct PanelParams {
   double* P;  // panel (mp x b), column-major
   int64_t ld;

@@ -20,12 +20,12 @@ namespace hb {
 namespace {
 
 template <typename P>
-void coop(void (*kern)(P), int grid, size_t smem, cudaStream_t st, P prm) {
+void coop(void (*kern)(P), int grid, size_t smem, cudaStream_t st, P prm, int threads = 256) {
   void* args[] = {&prm};
-  if (smem > 48 * 1024)
+  if (smem > 32 * 1024)  // opt in well below 48 KB: static shared memory counts too
     HB_CUDA(cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem));
-  HB_CUDA(cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(256), args, smem, st));
+  HB_CUDA(cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(threads), args, smem, st));
   launch_counter().fetch_add(1);
 }
 
@@ -64,8 +64,8 @@ void build_T(hb_context* c, const double* V, int64_t ldv, int64_t mp, int b, con
   g.M = b; g.N = b; g.K = mp; g.alpha = 1.0; g.A = V; g.lda = ldv; g.transA = true;
   g.B = V; g.ldb = ldv; g.beta = 0.0; g.C = S; g.ldc = b;
   Gemm{c}(g);
-  const size_t tsm = (size_t)b * b * sizeof(double);
-  if (tsm > 48 * 1024)
+  const size_t tsm = ((size_t)b * b + (size_t)b * (b - 1) / 2) * sizeof(double);
+  if (tsm > 32 * 1024)  // opt in well below 48 KB: static shared memory counts too
     HB_CUDA(cudaFuncSetAttribute((const void*)build_T_kernel,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm));
   build_T_kernel<<<1, 128, tsm, c->stream>>>(S, b, tau, b, T, b);
@@ -80,11 +80,16 @@ void panel_and_T(hb_context* c, double* P, int64_t ld, int64_t mp, int b, double
                  double* tau, double* T) {
   cudaStream_t st = c->stream;
   double* slots = ws<double>(c, B_SLOTS, (size_t)c->num_sms * (kBlockMax + 1) * 2 + 64);
-  double* scal2 = ws<double>(c, B_PSCAL, 8);
-  const int G = clampi(ceil_div(mp, 64), 1, c->coop_sms);
+  double* scal2 = ws<double>(c, B_PSCAL, 2 * kBlockMax + 8);
+  // as few CTAs as shared memory allows (~150 KB of panel per CTA): fewer partials to reduce and
+  // cheaper grid barriers per column
+  auto panel_ctas = [&](int64_t rows, int cols) {
+    return clampi(ceil_div(rows * cols * 8, 150 * 1024), 1, c->coop_sms);
+  };
+  const int G = panel_ctas(mp, b);
   const int64_t chunk = ceil_div(mp, G);
   const int64_t budget = (200 * 1024) / 8;  // doubles of shared memory per CTA
-  int bsub = (int)std::min<int64_t>(b, budget / (chunk + 2) - 1);
+  int bsub = (int)std::min<int64_t>(b, budget / (chunk + 3));
   if (bsub >= 8 && bsub < b) bsub &= ~7;
   if (bsub < 8 && bsub < b) {
     // very tall panel: global-memory fallback kernel
@@ -113,13 +118,13 @@ void panel_and_T(hb_context* c, double* P, int64_t ld, int64_t mp, int b, double
     }
     PanelParams pp{};
     pp.P = P + c0 + c0 * ld; pp.ld = ld; pp.mp = mps; pp.b = bs;
-    const int Gs = clampi(ceil_div(mps, 64), 1, c->coop_sms);
+    const int Gs = panel_ctas(mps, bs);
     pp.chunk = ceil_div(mps, Gs);
     pp.tau = tau + c0; pp.V = V + c0 + c0 * ldv; pp.ldv = ldv;
-    pp.nslot = slots; pp.wslot = slots + c->num_sms; pp.scal = scal2;
+    pp.nslot = nullptr; pp.wslot = slots; pp.scal = scal2;  // [2][Gs][bs] partials, [2][bs] rows
     pp.bar = barrier(c);
-    const size_t smem = ((size_t)bs * (pp.chunk + 1) + bs) * sizeof(double);
-    coop(panel_qr_smem_kernel, Gs, smem, st, pp);
+    const size_t smem = ((size_t)bs * (pp.chunk + 1) + 2 * bs) * sizeof(double);
+    coop(panel_qr_smem_kernel, Gs, smem, st, pp, kPanelThreads);
     if (c0 + bs < b) {
       build_T(c, V + c0 + c0 * ldv, ldv, mps, bs, tau + c0, Tsub, B_S);
       apply_block_reflector(c, V + c0 + c0 * ldv, ldv, Tsub, bs, P + c0 + (c0 + bs) * ld, ld, mps,
@@ -442,8 +447,8 @@ void rank_matrix_inplace(hb_context* c, double* A, int64_t m, int64_t n, int64_t
       }
       if (n2 > 0) {
         Phase ph(c, HB_PH_DOWNDATE);
-        const size_t rsm = (size_t)bh * bh * sizeof(double);
-        if (rsm > 48 * 1024)
+        const size_t rsm = ((size_t)bh * (bh + 1) / 2 + (size_t)bh * ell) * sizeof(double);
+        if (rsm > 32 * 1024)  // opt in well below 48 KB: static shared memory counts too
           HB_CUDA(cudaFuncSetAttribute((const void*)sketch_trsm_kernel,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm));
         sketch_trsm_kernel<<<1, ell, rsm, st>>>(Y + j * ell, ell, ell, P, lda, bh, Z, ell);
