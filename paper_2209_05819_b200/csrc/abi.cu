@@ -465,7 +465,16 @@ void hb_sweep_release(void) {
 
 static constexpr int64_t kSmallN = 16384;   // problems up to this N ...
 static constexpr double kSmallRank = 1000.0; // ... and this predicted rank share the GPU ...
-static constexpr int kSubStreams = 4;      // ... on this many concurrent streams
+static constexpr int kSubStreams = 4;      // ... on this many concurrent streams (HB_SUBSTREAMS)
+
+static int sub_streams() {
+  static const int n = [] {
+    const char* e = getenv("HB_SUBSTREAMS");
+    const int v = e ? atoi(e) : kSubStreams;
+    return v < 1 ? 1 : (v > 16 ? 16 : v);
+  }();
+  return n;
+}
 
 hb_status hb_sweep_ex(const hb_problem* probs, int64_t n, const int32_t* devices, int32_t ndev,
                       hb_rank_result* out, int32_t* status_out, hb_sweep_opts* opts) {
@@ -520,7 +529,7 @@ hb_status hb_sweep_ex(const hb_problem* probs, int64_t n, const int32_t* devices
       cudaEvent_t ready;
       cudaEventCreateWithFlags(&ready, cudaEventDisableTiming);
       cudaEventRecord(ready, c->stream);
-      const int nsub = (int)std::min<size_t>(kSubStreams, small.size());
+      const int nsub = (int)std::min<size_t>(sub_streams(), small.size());
       std::vector<std::thread> sth;
       std::mutex sub_mu;
       auto sub_worker = [&](int s) {

@@ -370,14 +370,28 @@ static int64_t tiles_of(int64_t M, int64_t N, int64_t K) {
   return ceil_div(M, bm) * ceil_div(N, bn);
 }
 
+// Split-K count from a wave model: a 64x64 tile costs ~kTileKNs per k at 3 CTAs/SM, a grid of
+// `tiles * s` CTAs runs in ceil(tiles * s / (3 * SMs)) waves of K/s each, and the split adds one
+// pass over (s + 1) M x N partials.  Skinny-M, long-K shapes (Ω·A, Vᵀ·A2 with M <= 128) have only
+// ~1.1 waves of tiles and gain ~1.6x from it.
 static int choose_slices(int64_t M, int64_t N, int64_t K, int num_sms, int64_t ws_elems) {
   const int64_t tiles = tiles_of(M, N, K);
-  if (tiles >= num_sms || K < 1024) return 1;
-  int64_t s = ceil_div(2 * (int64_t)num_sms, tiles);
-  s = std::min<int64_t>(s, K / 512);
-  s = std::min<int64_t>(s, 32);
-  while (s > 1 && s * M * N > ws_elems) --s;
-  return (int)std::max<int64_t>(s, 1);
+  const int64_t slots = 3ll * num_sms;
+  if (K < 1024 || tiles >= 8 * slots) return 1;
+  constexpr double kTileKNs = 98.6;         // 2*64*64 flop / (36.9 TF/s / 148 / 3)
+  constexpr double kBytesPerNs = 5000.0;    // ~HBM rate for the partial pass
+  constexpr double kReduceLaunchNs = 5000.0;
+  double best_t = (double)ceil_div(tiles, slots) * K * kTileKNs;
+  int best = 1;
+  for (int s = 2; s <= 32; ++s) {
+    if (K / s < 256 || (int64_t)s * M * N > ws_elems) break;
+    const int64_t kc = round_up(ceil_div(K, s), 16);
+    const int64_t se = ceil_div(K, kc);
+    const double t = (double)ceil_div(tiles * se, slots) * kc * kTileKNs +
+                     (double)(se + 1) * M * N * 8.0 / kBytesPerNs + kReduceLaunchNs;
+    if (t < 0.97 * best_t) { best_t = t; best = s; }
+  }
+  return best;
 }
 
 int64_t gemm_fro_count(int64_t M, int64_t N, int64_t K) {
@@ -428,6 +442,9 @@ void launch_dgemm(const GemmArgs& g, double* ws, int64_t ws_elems, int num_sms, 
     p.partial = ws;
     splitk_reduce<<<kReduceBlocks, 256, 0, st>>>(p, s_eff);
     HB_LAUNCH_CHECK();
+    const int64_t cnt = gemm_fro_count(g.M, g.N, g.K);
+    if (g.fro_partials && cnt > kReduceBlocks)
+      HB_CUDA(cudaMemsetAsync(g.fro_partials + kReduceBlocks, 0, (cnt - kReduceBlocks) * sizeof(double), st));
   } else if (g.fro_partials) {
     // pad the partial array to the fixed count with zeros so the consumer can always sum
     // gemm_fro_count(M, N) entries

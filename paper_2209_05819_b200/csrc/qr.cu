@@ -397,56 +397,139 @@ __global__ void __launch_bounds__(256) panel_qr_kernel(PanelParams p) {
     for (int q = nref + tid; q < b; q += 256) p.tau[q] = 0.0;
 }
 
-// T of the compact-WY form from S = VᵀV and τ (LAPACK dlarft, forward/columnwise):
-// T[0:c, c] = −τ_c · T[0:c, 0:c] · S[0:c, c].  S's strict upper triangle (packed) and T live in
-// shared memory; step c is a triangular mat-vec split over threads.
+// T of the compact-WY form from S = VᵀV and τ (LAPACK dlarft, forward/columnwise), built by
+// recursive merging instead of the column recurrence T[0:c, c] = −τ_c·T[0:c,0:c]·S[0:c, c]
+// (whose b dependent steps made this a ~250 µs latency chain at b = 120):
+//   leaves: 8-column diagonal blocks by the recurrence (one warp each);
+//   level w: adjacent blocks [a, m) and [m, e) merge with T12 = −T1·S12·T2, all merges of a level
+//   in parallel (W = S12·T2 is parked, transposed, in T's unused lower-left block).
+// S's strict upper triangle (packed) and T live in shared memory.
 __global__ void build_T_kernel(const double* __restrict__ S, int64_t lds, const double* __restrict__ tau,
                                int b, double* __restrict__ T, int64_t ldt) {
   extern __shared__ double smT[];
-  double* Ts = smT;                       // b x b, column-major, ld b
-  double* Sp = smT + (size_t)b * b;       // packed strict upper: column c at c(c-1)/2
-  __shared__ double taus[kBlockMax];
-  const int t = threadIdx.x;
-  for (int e = t; e < b * b; e += blockDim.x) Ts[e] = 0.0;
-  for (int c = 1; c < b; ++c)
-    for (int k = t; k < c; k += blockDim.x) Sp[c * (c - 1) / 2 + k] = S[k + (int64_t)c * lds];
-  for (int c = t; c < b; c += blockDim.x) taus[c] = tau[c];
-  __syncthreads();
-  for (int c = 0; c < b; ++c) {
-    const double tc = taus[c];
-    const double* sc = Sp + c * (c - 1) / 2;
-    for (int r = t; r < c; r += blockDim.x) {
-      double s = 0.0;
-      for (int k = r; k < c; ++k) s += Ts[r + k * b] * sc[k];
-      Ts[r + c * b] = -tc * s;
+  const int ldT = b + 1;
+  double* Ts = smT;                        // b x b, column-major, ld b+1
+  double* Sp = smT + (size_t)b * ldT;      // packed strict upper: (r, c), r < c at c(c-1)/2 + r
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
+  auto sp = [&](int r, int c) { return Sp[c * (c - 1) / 2 + r]; };
+  for (int e = tid; e < b * ldT; e += nt) Ts[e] = 0.0;
+  {
+    constexpr int U = 8;
+    const int tot = b * b;
+    for (int e0 = tid; e0 < tot; e0 += nt * U) {
+      double v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int e = e0 + u * nt;
+        const int r = e % b, c = e / b;
+        v[u] = (e < tot && r < c) ? S[r + (int64_t)c * lds] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int e = e0 + u * nt;
+        const int r = e % b, c = e / b;
+        if (e < tot && r < c) Sp[c * (c - 1) / 2 + r] = v[u];
+      }
     }
-    if (t == 0) Ts[c + c * b] = tc;
+  }
+  __syncthreads();
+  // leaves
+  for (int L = warp; L * 8 < b; L += nw) {
+    const int a = L * 8, n8 = min(8, b - a);
+    for (int c = 0; c < n8; ++c) {
+      const double tc = tau[a + c];
+      if (lane < c) {
+        double s = 0.0;
+        for (int k = lane; k < c; ++k) s += Ts[(a + lane) + (a + k) * ldT] * sp(a + k, a + c);
+        Ts[(a + lane) + (a + c) * ldT] = -tc * s;
+      } else if (lane == c) {
+        Ts[(a + c) + (a + c) * ldT] = tc;
+      }
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  for (int w = 8; w < b; w *= 2) {
+    const int nm = (b + 2 * w - 1) / (2 * w);
+    const int per = w * w;
+    // W[r][j] = Σ_{k<=j} S12[r][k]·T2[k][j]  -> Ts[(m+j) + (a+r)·ldT]
+    for (int e = tid; e < nm * per; e += nt) {
+      const int i = e / per, rem = e % per, r = rem % w, j = rem / w;
+      const int a = 2 * w * i, m = min(a + w, b), ee = min(a + 2 * w, b);
+      if (a + r >= m || m + j >= ee) continue;
+      double s = 0.0;
+      for (int k = 0; k <= j; ++k) s += sp(a + r, m + k) * Ts[(m + k) + (m + j) * ldT];
+      Ts[(m + j) + (a + r) * ldT] = s;
+    }
+    __syncthreads();
+    // T12[r][j] = −Σ_{k>=r} T1[r][k]·W[k][j]
+    for (int e = tid; e < nm * per; e += nt) {
+      const int i = e / per, rem = e % per, r = rem % w, j = rem / w;
+      const int a = 2 * w * i, m = min(a + w, b), ee = min(a + 2 * w, b);
+      if (a + r >= m || m + j >= ee) continue;
+      double s = 0.0;
+      for (int k = r; k < m - a; ++k) s += Ts[(a + r) + (a + k) * ldT] * Ts[(m + j) + (a + k) * ldT];
+      Ts[(a + r) + (m + j) * ldT] = -s;
+    }
     __syncthreads();
   }
-  for (int e = t; e < b * b; e += blockDim.x) T[(e % b) + (int64_t)(e / b) * ldt] = Ts[e];
+  for (int e = tid; e < b * b; e += nt) {
+    const int r = e % b, c = e / b;
+    T[r + (int64_t)c * ldt] = r <= c ? Ts[r + c * ldT] : 0.0;
+  }
 }
 
-// Z (ell x b) = Y1 R11^{-1}: row-wise forward substitution, one thread per sketch row; R11's
-// upper triangle (packed) and Z are kept in shared memory.
+// Z (ell x b) = Y1 R11^{-1}: one thread per sketch row, 8 columns at a time (8 independent FMA
+// chains per thread).  R11 is staged in shared memory as row-major 8-column strips
+// (strip B holds R[0:8B+8, 8B:8B+8] at offset 32·B·(B+1)), Z as Zs[c·ell + t].
 __global__ void sketch_trsm_kernel(const double* __restrict__ Y1, int64_t ldy, int ell,
                                    const double* __restrict__ R, int64_t ldr, int b,
                                    double* __restrict__ Z, int64_t ldz) {
   extern __shared__ double smZ[];
-  double* Rp = smZ;                              // packed upper incl. diagonal: column c at c(c+1)/2
-  double* Zs = smZ + (size_t)b * (b + 1) / 2;    // b x ell, Zs[c * ell + t]
-  for (int c = 0; c < b; ++c)
-    for (int i = threadIdx.x; i <= c; i += blockDim.x) Rp[c * (c + 1) / 2 + i] = R[i + (int64_t)c * ldr];
+  const int nb8 = (b + 7) / 8;
+  double* Rs = smZ;                                  // 32·nb8·(nb8+1) doubles
+  double* Zs = smZ + (size_t)32 * nb8 * (nb8 + 1);   // b x ell
+  const int t = threadIdx.x, nt = blockDim.x;
+  for (int B = 0; B < nb8; ++B) {
+    double* strip = Rs + 32 * B * (B + 1);
+    const int rows = 8 * B + 8;
+    for (int e = t; e < rows * 8; e += nt) {
+      const int i = e >> 3, jj = e & 7, c = 8 * B + jj;
+      double v;
+      if (c >= b) v = (i == c) ? 1.0 : 0.0;          // padding column: identity
+      else v = (i <= c) ? R[i + (int64_t)c * ldr] : 0.0;
+      strip[e] = v;
+    }
+  }
   __syncthreads();
-  const int t = threadIdx.x;
   if (t >= ell) return;
-  for (int c = 0; c < b; ++c) {
-    const double* rc = Rp + c * (c + 1) / 2;
-    double s = Y1[t + (int64_t)c * ldy];
-    for (int i = 0; i < c; ++i) s -= Zs[i * ell + t] * rc[i];
-    const double d = rc[c];
-    const double z = d != 0.0 ? s / d : 0.0;
-    Zs[c * ell + t] = z;
-    Z[t + (int64_t)c * ldz] = z;
+  for (int B = 0; B < nb8; ++B) {
+    const int a = 8 * B;
+    const double* strip = Rs + 32 * B * (B + 1);
+    double acc[8];
+#pragma unroll
+    for (int jj = 0; jj < 8; ++jj) acc[jj] = (a + jj < b) ? Y1[t + (int64_t)(a + jj) * ldy] : 0.0;
+    for (int i = 0; i < a; ++i) {
+      const double z = Zs[i * ell + t];
+      const double2* r2 = reinterpret_cast<const double2*>(strip + i * 8);
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        const double2 rv = r2[h];
+        acc[2 * h] = fma(-z, rv.x, acc[2 * h]);
+        acc[2 * h + 1] = fma(-z, rv.y, acc[2 * h + 1]);
+      }
+    }
+#pragma unroll
+    for (int jj = 0; jj < 8; ++jj) {
+      const double d = strip[(a + jj) * 8 + jj];
+      const double z = d != 0.0 ? acc[jj] / d : 0.0;
+#pragma unroll
+      for (int j2 = jj + 1; j2 < 8; ++j2) acc[j2] = fma(-z, strip[(a + jj) * 8 + j2], acc[j2]);
+      if (a + jj < b) {
+        Zs[(a + jj) * ell + t] = z;
+        Z[t + (int64_t)(a + jj) * ldz] = z;
+      }
+    }
   }
 }
 

@@ -49,7 +49,7 @@ struct Gemm {
     if (c->profiling)
       c->marks.push_back({PH_GEMM, e0, prof_event(c), 2.0 * (double)g.M * (double)g.N * (double)g.K});
   }
-  static constexpr int64_t kSplitKElems = 8ll << 20;
+  static constexpr int64_t kSplitKElems = 24ll << 20;  // 192 MB of split-K partials
 };
 
 // Householder panel + compact-WY T.  Panel mp x b at P (ld); V (ld ldv) and T (ld b) out.
@@ -64,11 +64,11 @@ void build_T(hb_context* c, const double* V, int64_t ldv, int64_t mp, int b, con
   g.M = b; g.N = b; g.K = mp; g.alpha = 1.0; g.A = V; g.lda = ldv; g.transA = true;
   g.B = V; g.ldb = ldv; g.beta = 0.0; g.C = S; g.ldc = b;
   Gemm{c}(g);
-  const size_t tsm = ((size_t)b * b + (size_t)b * (b - 1) / 2) * sizeof(double);
+  const size_t tsm = ((size_t)b * (b + 1) + (size_t)b * (b - 1) / 2) * sizeof(double);
   if (tsm > 32 * 1024)  // opt in well below 48 KB: static shared memory counts too
     HB_CUDA(cudaFuncSetAttribute((const void*)build_T_kernel,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm));
-  build_T_kernel<<<1, 128, tsm, c->stream>>>(S, b, tau, b, T, b);
+  build_T_kernel<<<1, 256, tsm, c->stream>>>(S, b, tau, b, T, b);
   HB_LAUNCH_CHECK();
 }
 
@@ -447,7 +447,8 @@ void rank_matrix_inplace(hb_context* c, double* A, int64_t m, int64_t n, int64_t
       }
       if (n2 > 0) {
         Phase ph(c, HB_PH_DOWNDATE);
-        const size_t rsm = ((size_t)bh * (bh + 1) / 2 + (size_t)bh * ell) * sizeof(double);
+        const int nb8 = (bh + 7) / 8;
+        const size_t rsm = ((size_t)32 * nb8 * (nb8 + 1) + (size_t)bh * ell) * sizeof(double);
         if (rsm > 32 * 1024)  // opt in well below 48 KB: static shared memory counts too
           HB_CUDA(cudaFuncSetAttribute((const void*)sketch_trsm_kernel,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm));

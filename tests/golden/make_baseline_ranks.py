@@ -6,7 +6,9 @@ problem_seed(0, d, d', N), tolerances 1e-12 (and 1e-10 for d = 4).  Ranks come f
 (oracle/oracle.py: C entry restatement + LAPACK gesdd); every record stores σ₁, σ_p, σ_{p+1}
 and the boundary gap so that a GPU mismatch can be judged against it.
 
-Usage: python tests/golden/make_baseline_ranks.py [max_N]   (default 4000; 8000 takes ~1 h on 8 cores)
+Usage: python tests/golden/make_baseline_ranks.py [max_N] [d:kernel]
+  (default 4000; 8000 takes ~1 h on 8 cores; "2:log_r" restricts to one dimension and kernel,
+  used for the configs[1] N = 16000 entries)
 Runs anywhere the oracle builds (no GPU, no /root/reference needed); results are merged into the
 existing JSON so larger N can be added incrementally.
 """
@@ -33,13 +35,18 @@ def geometries():
 
 def main() -> int:
     max_n = int(sys.argv[1]) if len(sys.argv) > 1 else 4000
+    only = sys.argv[2].split(":") if len(sys.argv) > 2 else None
     recs = json.loads(OUT.read_text()) if OUT.exists() else []
     have = {(r["d"], r["dprime"], r["kernel"], r["N"]) for r in recs}
     for n in [x for x in NS if x <= max_n]:
         for d, dp in geometries():
             seed = O.problem_seed(0, d, dp, n)
             x, y = O.pair_points(d, dp, n, O.UNIFORM, seed)
+            if only and d != int(only[0]):
+                continue
             for kname in KERNELS:
+                if only and kname != only[1]:
+                    continue
                 if (d, dp, kname, n) in have:
                     continue
                 tols = [1e-12, 1e-10] if d == 4 else [1e-12]
