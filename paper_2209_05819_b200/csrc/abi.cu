@@ -525,28 +525,40 @@ hb_status hb_sweep_ex(const hb_problem* probs, int64_t n, const int32_t* devices
     }
     std::vector<hb_context*> subs;
     if (!small.empty()) {
-      std::atomic<size_t> next{0};
+      std::atomic<size_t> next{0};  // set to nsub below: sub-stream s starts with small[s]
       cudaEvent_t ready;
       cudaEventCreateWithFlags(&ready, cudaEventDisableTiming);
       cudaEventRecord(ready, c->stream);
       const int nsub = (int)std::min<size_t>(sub_streams(), small.size());
+      next = (size_t)nsub;
       std::vector<std::thread> sth;
       std::mutex sub_mu;
       auto sub_worker = [&](int s) {
         hb_status ss = HB_OK;
         hb_context* sc = cached_context(devices[w], 1000 + slot[w] * 16 + s, &ss);
         if (!sc) {
-          for (size_t q = next.fetch_add(1); q < small.size(); q = next.fetch_add(1)) st[small[q]] = ss;
+          for (size_t q = (size_t)s; q < small.size(); q = next.fetch_add(1)) st[small[q]] = ss;
           return;
         }
         {
           std::lock_guard<std::mutex> lk(sub_mu);
           subs.push_back(sc);
         }
-        sc->coop_sms = std::max(1, c->num_sms / nsub);
+        // stream 0 runs the costliest small problem (the critical path of the group) at high
+        // stream priority with half of the SMs for its cooperative grids; the others share the
+        // rest (caps sum to <= num_sms, so co-resident barriers cannot deadlock)
+        int lo = 0, hi = 0;
+        cudaDeviceGetStreamPriorityRange(&lo, &hi);
+        try {
+          hb::context_set_priority(sc, (s == 0 && nsub > 1) ? hi : lo);
+        } catch (const hb::Error&) {
+        }
+        const int half = c->num_sms / 2;
+        sc->coop_sms = nsub == 1 ? c->num_sms
+                                 : (s == 0 ? half : std::max(1, (c->num_sms - half) / (nsub - 1)));
         sc->profiling = c->profiling;
         cudaStreamWaitEvent(sc->stream, ready, 0);
-        for (size_t q = next.fetch_add(1); q < small.size(); q = next.fetch_add(1)) {
+        for (size_t q = (size_t)s; q < small.size(); q = next.fetch_add(1)) {
           const hb_problem& p = probs[small[q]];
           st[small[q]] = hb_rank(sc, &p.kernel, &p.pair, p.tols, p.ntol, out + offset[small[q]]);
         }

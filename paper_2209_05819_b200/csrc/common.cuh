@@ -5,6 +5,8 @@
 #include <stdint.h>
 
 #include <atomic>
+#include <map>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 
@@ -26,6 +28,22 @@ struct Error : std::runtime_error {
                         std::string(#x) + ": " + cudaGetErrorString(e_) + " @" __FILE__ ":" + \
                             std::to_string(__LINE__));                                       \
   } while (0)
+
+// Raise (never lower) a kernel's dynamic shared-memory limit on the current device.  Host threads
+// (hb_sweep workers, concurrent sub-streams) launch the same kernels with different sizes: an
+// attribute lowered between another thread's set and launch fails that launch ("too many resources
+// requested" / "invalid argument").  Monotonic updates under one lock make that impossible.
+inline void ensure_dyn_smem(const void* kern, size_t bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, size_t> cur;
+  int dev = 0;
+  HB_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  size_t& c = cur[{dev, kern}];
+  if (c >= bytes) return;
+  HB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  c = bytes;
+}
 
 // every kernel launch site of the library passes through here: the counter backs the
 // "gpu_launches" figure of bench.py (hb_stats.launches)

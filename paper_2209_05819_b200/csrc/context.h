@@ -13,6 +13,7 @@ struct hb_context {
   cudaStream_t stream = nullptr;
   int num_sms = 148;
   int coop_sms = 148;  // SM share for cooperative grids (< num_sms when streams run concurrently)
+  int priority = 0;    // CUDA stream priority of `stream` (0 = default)
   int block_max = hb::kBlockMax;
   bool spectral = false;  // spectral (probabilistic) stopping test (off: measured +3% columns saved for 7% time)
   double eta = 0.05;  // first stop once ||A22||_F <= eta * tol * sigma1 (refined if a bracket stays open)
@@ -91,6 +92,7 @@ void rank_matrix_inplace(hb_context* c, double* A, int64_t m, int64_t n, int64_t
                          const double* tols, int ntol, hb_rank_result* out, float* fact_ms,
                          float* cert_ms);
 void context_init(hb_context* c, int device);
+void context_set_priority(hb_context* c, int prio);
 void context_free(hb_context* c);
 
 }  // namespace hb

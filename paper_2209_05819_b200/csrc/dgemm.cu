@@ -334,14 +334,13 @@ static void run_cfg(const GemmParams& p, int slices, bool vec, cudaStream_t st) 
   using C_ = Cfg<TA, WARPS_M, WARPS_N, WM, WN, BK_, ST_>;
   dim3 grid((unsigned)ceil_div(p.M, C_::BM), (unsigned)ceil_div(p.N, C_::BN), (unsigned)slices);
   HB_REQUIRE(grid.y <= 65535u && grid.z <= 65535u, HB_ECAP, "dgemm: grid too large");
-  // the attribute is per device; setting it on every launch costs ~1 µs of host time
   if (vec) {
     auto k = dgemm_kernel<TA, WARPS_M, WARPS_N, WM, WN, true, BK_, ST_>;
-    HB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C_::SMEM));
+    ensure_dyn_smem((const void*)k, C_::SMEM);
     k<<<grid, C_::NT, C_::SMEM, st>>>(p);
   } else {
     auto k = dgemm_kernel<TA, WARPS_M, WARPS_N, WM, WN, false, BK_, ST_>;
-    HB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C_::SMEM));
+    ensure_dyn_smem((const void*)k, C_::SMEM);
     k<<<grid, C_::NT, C_::SMEM, st>>>(p);
   }
   HB_LAUNCH_CHECK();

@@ -22,9 +22,7 @@ namespace {
 template <typename P>
 void coop(void (*kern)(P), int grid, size_t smem, cudaStream_t st, P prm, int threads = 256) {
   void* args[] = {&prm};
-  if (smem > 32 * 1024)  // opt in well below 48 KB: static shared memory counts too
-    HB_CUDA(cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem));
+  ensure_dyn_smem((const void*)kern, smem);
   HB_CUDA(cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(threads), args, smem, st));
   launch_counter().fetch_add(1);
 }
@@ -65,9 +63,7 @@ void build_T(hb_context* c, const double* V, int64_t ldv, int64_t mp, int b, con
   g.B = V; g.ldb = ldv; g.beta = 0.0; g.C = S; g.ldc = b;
   Gemm{c}(g);
   const size_t tsm = ((size_t)b * (b + 1) + (size_t)b * (b - 1) / 2) * sizeof(double);
-  if (tsm > 32 * 1024)  // opt in well below 48 KB: static shared memory counts too
-    HB_CUDA(cudaFuncSetAttribute((const void*)build_T_kernel,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm));
+  ensure_dyn_smem((const void*)build_T_kernel, tsm);
   build_T_kernel<<<1, 256, tsm, c->stream>>>(S, b, tau, b, T, b);
   HB_LAUNCH_CHECK();
 }
@@ -264,8 +260,7 @@ void two_stage_bidiag(hb_context* c, double* Mk, int64_t ldm, int64_t k, double*
   cudaStream_t st = c->stream;
   if (k <= kSmallBidiag) {  // one CTA, whole triangle in shared memory
     const size_t smem = ((size_t)k * (k + 1) + 3 * (size_t)k) * sizeof(double);
-    HB_CUDA(cudaFuncSetAttribute((const void*)bidiag_small_kernel,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    ensure_dyn_smem((const void*)bidiag_small_kernel, smem);
     bidiag_small_kernel<<<1, 256, smem, st>>>(Mk, ldm, (int)k, d, e);
     HB_LAUNCH_CHECK();
     return;
@@ -449,9 +444,7 @@ void rank_matrix_inplace(hb_context* c, double* A, int64_t m, int64_t n, int64_t
         Phase ph(c, HB_PH_DOWNDATE);
         const int nb8 = (bh + 7) / 8;
         const size_t rsm = ((size_t)32 * nb8 * (nb8 + 1) + (size_t)bh * ell) * sizeof(double);
-        if (rsm > 32 * 1024)  // opt in well below 48 KB: static shared memory counts too
-          HB_CUDA(cudaFuncSetAttribute((const void*)sketch_trsm_kernel,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm));
+        ensure_dyn_smem((const void*)sketch_trsm_kernel, rsm);
         sketch_trsm_kernel<<<1, ell, rsm, st>>>(Y + j * ell, ell, ell, P, lda, bh, Z, ell);
         HB_LAUNCH_CHECK();
         GemmArgs g{};
@@ -654,6 +647,19 @@ void context_init(hb_context* c, int device) {
   HB_CUDA(cudaMallocHost(&c->pinned, 4096));
   for (auto& e : c->ev) HB_CUDA(cudaEventCreate(&e));
   c->bufs.resize(B_COUNT);
+}
+
+// Re-create the context stream with another CUDA priority (workspace stays allocated: it was
+// allocated stream-ordered, and the old stream is drained first).
+void context_set_priority(hb_context* c, int prio) {
+  if (c->priority == prio) return;
+  HB_CUDA(cudaSetDevice(c->device));
+  cudaStream_t s = nullptr;
+  HB_CUDA(cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, prio));
+  HB_CUDA(cudaStreamSynchronize(c->stream));
+  HB_CUDA(cudaStreamDestroy(c->stream));
+  c->stream = s;
+  c->priority = prio;
 }
 
 void context_free(hb_context* c) {
