@@ -103,6 +103,13 @@ __global__ void band_bidiag_out(const double* Bd, int64_t k, int nb, double* d, 
 __global__ void bulge_chase_kernel(double* Bd, int64_t k, int nb, int* prog);
 __global__ void bidiag_small_kernel(const double* Mk, int64_t ldm, int k, double* d, double* e);
 constexpr int kSmallBidiag = 144;  // k x k triangle up to this size: one-CTA shared-memory bidiag
+// Mid-size k: one thread-block cluster holds the triangle in distributed shared memory
+// (bidiag_cluster.cu).  bidiag_cluster_size(k) = cluster size to use (8 or 16), 0 = does not fit.
+constexpr size_t kBidiagClusterSmem = 225 * 1024;
+size_t bidiag_cluster_smem(int k, int G);
+int bidiag_cluster_size(int k);
+void launch_bidiag_cluster(const double* Mk, int64_t ldm, int k, double* d, double* e, int G,
+                           cudaStream_t st);
 __global__ void sigma_queries_kernel(const double* d, const double* e, int64_t k,
                                      const SigmaQuery* q, int nq, SigmaAnswer* out);
 __global__ void sigma_all_kernel(const double* d, const double* e, int64_t k, double sigma_max,

@@ -265,6 +265,10 @@ void two_stage_bidiag(hb_context* c, double* Mk, int64_t ldm, int64_t k, double*
     HB_LAUNCH_CHECK();
     return;
   }
+  if (const int G = bidiag_cluster_size((int)k)) {  // one cluster, triangle in DSMEM
+    launch_bidiag_cluster(Mk, ldm, (int)k, d, e, G, st);
+    return;
+  }
   const int64_t ldp = round_up(k, 8);
   double* P2 = ws<double>(c, B_ST1_P, (size_t)ldp * kBand);
   double* X = ws<double>(c, B_ST1_X, (size_t)ldp * kBand);

@@ -62,6 +62,23 @@ def test_sigma_values_match_lapack(ctx, hb, oracle):
     np.testing.assert_allclose(sg[:300], so[:300], rtol=1e-9, atol=1e-13 * so[0])
 
 
+@pytest.mark.parametrize("k", [145, 200, 368, 421, 600, 700])
+def test_certification_sigma_all_bidiag_paths(ctx, oracle, k):
+    """σ(R_k) of a full-rank k x k matrix through each bidiagonalisation path (k <= 144 one CTA,
+    cluster DSMEM up to ~600, two-stage above) against LAPACK, and the rank against the oracle."""
+    rng = np.random.default_rng(k)
+    q1, _ = np.linalg.qr(rng.standard_normal((k, k)))
+    q2, _ = np.linalg.qr(rng.standard_normal((k, k)))
+    s = np.logspace(0, -9, k)
+    M = (q1 * s) @ q2.T
+    r = rank_dense(ctx, M, [1e-12, 1e-6])
+    so = np.linalg.svd(M, compute_uv=False)
+    assert [x.rank for x in r] == [oracle.epsilon_rank_from_sigma(so, t).rank for t in (1e-12, 1e-6)]
+    sg = np.array(ctx.last_sigma(k))
+    assert len(sg) == r[0].k_factored
+    np.testing.assert_allclose(sg[: len(sg)], so[: len(sg)], rtol=1e-9, atol=1e-14 * so[0])
+
+
 def _paper_cases(tables, max_n):
     for tab in tables:
         for row in tab["rows"]:
