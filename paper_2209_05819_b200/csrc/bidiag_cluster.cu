@@ -72,7 +72,7 @@ __global__ void __launch_bounds__(kBdThreads) bidiag_cluster_kernel(const double
     const int c = g + jl * G;
     for (int r = lane; r < k; r += 32) M[jl * ld + r] = r <= c ? Mk[r + (int64_t)c * ldm] : 0.0;
   }
-  __syncthreads();
+  cl.sync();  // every CTA of the cluster is running before any DSMEM access
   // column 0 (owned by CTA 0) to every CTA's col[0]
   if (g == 0)
     for (int idx = tid; idx < k * G; idx += kBdThreads) {
@@ -264,6 +264,7 @@ void launch_bidiag_cluster(const double* Mk, int64_t ldm, int k, double* d, doub
   cfg.attrs = at; cfg.numAttrs = 1;
   HB_CUDA(cudaLaunchKernelEx(&cfg, bidiag_cluster_kernel, Mk, ldm, k, d, e));
   launch_counter().fetch_add(1, std::memory_order_relaxed);
+  if (sync_debug_enabled()) debug_sync_after_launch("bidiag_cluster", G);
 }
 
 }  // namespace hb

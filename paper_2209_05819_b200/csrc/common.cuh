@@ -5,6 +5,8 @@
 #include <stdint.h>
 
 #include <atomic>
+#include <cstdio>
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <stdexcept>
@@ -51,10 +53,19 @@ inline std::atomic<unsigned long long>& launch_counter() {
   static std::atomic<unsigned long long> n{0};
   return n;
 }
+// HB_SYNC_DEBUG=1: wait for every launch (device-wide, 10 s watchdog) and name the launch site
+// that did not finish — hang triage without a debugger.
+void debug_sync_after_launch(const char* file, int line);
+inline bool sync_debug_enabled() {
+  static const bool on = getenv("HB_SYNC_DEBUG") != nullptr;
+  return on;
+}
+
 #define HB_LAUNCH_CHECK()                                         \
   do {                                                            \
     ::hb::launch_counter().fetch_add(1, std::memory_order_relaxed); \
     HB_CUDA(cudaGetLastError());                                  \
+    if (::hb::sync_debug_enabled()) ::hb::debug_sync_after_launch(__FILE__, __LINE__); \
   } while (0)
 
 #define HB_REQUIRE(cond, st, msg) \
@@ -85,25 +96,58 @@ struct GridBarrier {
   unsigned int* gen;
 };
 
-__device__ __forceinline__ void grid_sync(GridBarrier b) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    volatile unsigned int* vgen = b.gen;
-    const unsigned int my_gen = *vgen;
-    __threadfence();
-    const unsigned int nb = gridDim.x * gridDim.y * gridDim.z;
-    const unsigned int arrived = atomicAdd(b.count, 1u);
-    if (arrived == nb - 1) {
-      *b.count = 0;
-      __threadfence();
-      atomicAdd(b.gen, 1u);
-    } else {
-      while (*vgen == my_gen) __nanosleep(20);
-    }
-    __threadfence();
-  }
-  __syncthreads();
+// Per-launch barrier handle: thread 0 of every CTA reads the generation once at kernel start (it
+// cannot advance before every CTA has arrived at the first barrier), so each barrier costs one
+// acq_rel atomic arrival plus acquire polling — no extra generation read per barrier.
+// (Same release/acquire pattern as CUTLASS's GenericBarrier.)
+__device__ __forceinline__ unsigned int ld_acquire_gpu(const unsigned int* p) {
+  unsigned int v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
 }
+__device__ __forceinline__ void st_release_gpu(unsigned int* p, unsigned int v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// acq_rel: the LAST arriver never polls `gen`, so its arrival must itself acquire the other
+// CTAs' writes (and drop stale L1 lines) — with a release-only arrival it read stale partials
+// and left the grid with diverging barrier counts (observed hang).
+__device__ __forceinline__ unsigned int atom_add_acq_rel_gpu(unsigned int* p, unsigned int v) {
+  unsigned int old;
+  asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+
+struct GridSync {
+  unsigned int* count;
+  unsigned int* gen;
+  unsigned int g;  // generation seen by thread 0
+  __device__ __forceinline__ explicit GridSync(GridBarrier b) : count(b.count), gen(b.gen), g(0) {
+    if (threadIdx.x == 0) g = ld_acquire_gpu(gen);
+  }
+  __device__ __forceinline__ void sync() {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const unsigned int nb = gridDim.x * gridDim.y * gridDim.z;
+      if (atom_add_acq_rel_gpu(count, 1u) == nb - 1) {
+        *count = 0;  // ordered before the generation bump by the release below
+        st_release_gpu(gen, g + 1);
+      } else {
+        unsigned int seen, spins = 0;
+        while ((seen = ld_acquire_gpu(gen)) == g) {
+          if (++spins == (1u << 26)) {
+            printf("[hb barrier] block %d of %d stuck: gen %u count %u\n", blockIdx.x, nb, seen,
+                   *(volatile unsigned int*)count);
+            __trap();
+          }
+        }
+        if (seen != g + 1)
+          printf("[hb barrier] block %d: generation jumped %u -> %u\n", blockIdx.x, g, seen);
+      }
+      ++g;
+    }
+    __syncthreads();
+  }
+};
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll

@@ -19,6 +19,7 @@ namespace hb {
 // and w_q = τ·vᵀP[:,q] = τ·(P[c,q] + g_q/(α − β)) without a second reduction, updates its rows,
 // and accumulates the partials of column c+1 in the same pass.
 __global__ void __launch_bounds__(kPanelThreads) panel_qr_smem_kernel(PanelParams p) {
+  GridSync gbar(p.bar);
   constexpr int NW = kPanelThreads / 32;
   extern __shared__ double psm[];
   __shared__ double red[NW][128];
@@ -55,7 +56,7 @@ __global__ void __launch_bounds__(kPanelThreads) panel_qr_smem_kernel(PanelParam
     if (r0 == 0 && rows > 0)
       for (int q = tid; q < b; q += kPanelThreads) rowc[q] = S[q * ldS];
   }
-  grid_sync(p.bar);
+  gbar.sync();
 
   for (int c = 0; c < nref; ++c) {
     const int par = c & 1;
@@ -143,7 +144,7 @@ __global__ void __launch_bounds__(kPanelThreads) panel_qr_smem_kernel(PanelParam
       }
     }
     if (!more) break;
-    grid_sync(p.bar);
+    gbar.sync();
   }
   // the last column(s) beyond nref (wide panels) were updated in place above
   for (int q = warp; q < b; q += NW) {

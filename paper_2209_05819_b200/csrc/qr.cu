@@ -51,6 +51,7 @@ __device__ __forceinline__ bool better(double na, int ia, double nb, int ib) {
 }
 
 __global__ void __launch_bounds__(256) sketch_cpqr_kernel(SketchParams p) {
+  GridSync gbar(p.bar);
   extern __shared__ double nrm_s[];  // norms of this CTA's columns (-1 = chosen)
   const int G = gridDim.x, g = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -98,7 +99,7 @@ __global__ void __launch_bounds__(256) sketch_cpqr_kernel(SketchParams p) {
     }
   };
   publish(0);
-  grid_sync(p.bar);
+  gbar.sync();
 
   int c = 0;
   for (; c < p.b_req; ++c) {
@@ -230,7 +231,7 @@ __global__ void __launch_bounds__(256) sketch_cpqr_kernel(SketchParams p) {
     }
     __syncthreads();
     publish((c + 1) & 1);
-    grid_sync(p.bar);
+    gbar.sync();
   }
   if (g == 0 && tid == 0) {
     // LAPACK-style swap list: swaps[i] = current position of the i-th pivot when it is
@@ -296,6 +297,7 @@ __global__ void permute_kernel(double* __restrict__ A, int64_t lda, int64_t m, d
 // panel_qr: Householder QR of the mp x b panel at P (column-major, ld).
 // ------------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) panel_qr_kernel(PanelParams p) {
+  GridSync gbar(p.bar);
   extern __shared__ double psm[];  // vs[chunk] | ws[b]
   const int G = gridDim.x, g = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -319,7 +321,7 @@ __global__ void __launch_bounds__(256) panel_qr_kernel(PanelParams p) {
     s = warp_sum(s);
     if (lane == 0) p.nslot[g] = s;
   }
-  grid_sync(p.bar);
+  gbar.sync();
 
   // reflectors for the first min(b, mp) columns (a wide panel, mp < b, occurs in the block LQ of
   // the band reduction); the remaining columns are only transformed
@@ -361,7 +363,7 @@ __global__ void __launch_bounds__(256) panel_qr_kernel(PanelParams p) {
       s = warp_sum(s);
       if (lane == 0) p.wslot[(size_t)g * b + q] = s;
     }
-    grid_sync(p.bar);
+    gbar.sync();
     for (int q = c + 1 + warp; q < b; q += 8) {
       const double s = warp_sum_strided(p.wslot + q, G, b);
       if (lane == 0) ws[q] = s * tau;
@@ -384,7 +386,7 @@ __global__ void __launch_bounds__(256) panel_qr_kernel(PanelParams p) {
     if (c + 1 >= b && tid == 0) p.nslot[g] = 0.0;
     if (c >= r0 && c < r1 && tid == 0) colc[c] = sh[2];
     if (g == 0 && tid == 0) p.tau[c] = tau;
-    grid_sync(p.bar);
+    gbar.sync();
   }
   // explicit V (unit diagonal, zeros above; zero columns beyond the last reflector)
   for (int q = warp; q < b; q += 8) {
@@ -536,6 +538,7 @@ __global__ void sketch_trsm_kernel(const double* __restrict__ Y1, int64_t ldy, i
 // σ₁ lower bound: power iteration on R_b = rows 0..b-1 of the factor (upper trapezoidal; the
 // strictly-lower part of the first b columns holds V and is masked).
 __global__ void __launch_bounds__(256) power_sigma1_kernel(PowerParams p) {
+  GridSync gbar(p.bar);
   const int G = gridDim.x, g = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int b = p.b;
@@ -595,7 +598,7 @@ __global__ void __launch_bounds__(256) power_sigma1_kernel(PowerParams p) {
       for (int w = 0; w < 8; ++w) s += ysum[w];
       sl[b] = s;
     }
-    grid_sync(p.bar);
+    gbar.sync();
   }
   if (g == 0 && tid == 0) *p.out = best;
 }

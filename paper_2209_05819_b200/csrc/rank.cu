@@ -25,6 +25,7 @@ void coop(void (*kern)(P), int grid, size_t smem, cudaStream_t st, P prm, int th
   ensure_dyn_smem((const void*)kern, smem);
   HB_CUDA(cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(threads), args, smem, st));
   launch_counter().fetch_add(1);
+  if (sync_debug_enabled()) debug_sync_after_launch("coop", grid);
 }
 
 int clampi(int64_t v, int lo, int hi) { return (int)std::max<int64_t>(lo, std::min<int64_t>(hi, v)); }
@@ -35,7 +36,7 @@ void sync_to_host(hb_context* c, const void* dsrc, void* hdst, size_t bytes) {
   std::memcpy(hdst, c->pinned, bytes);
 }
 
-GridBarrier barrier(hb_context* c) { return GridBarrier{c->bar, c->bar + 1}; }
+GridBarrier barrier(hb_context* c) { return GridBarrier{c->bar, c->bar + 32}; }  // separate 128 B lines
 
 struct Gemm {
   hb_context* c;
@@ -325,6 +326,7 @@ void two_stage_bidiag(hb_context* c, double* Mk, int64_t ldm, int64_t k, double*
     void* args[] = {&Bd, &kk, &kb, &prog};
     HB_CUDA(cudaLaunchCooperativeKernel((const void*)bulge_chase_kernel, dim3(G), dim3(256), args, 0, st));
     launch_counter().fetch_add(1);
+    if (sync_debug_enabled()) debug_sync_after_launch("bulge_chase", G);
   }
   band_bidiag_out<<<(unsigned)ceil_div(k, 256), 256, 0, st>>>(Bd, k, kBand, d, e);
   HB_LAUNCH_CHECK();
@@ -636,6 +638,13 @@ void prof_resolve(hb_context* c) {
   c->evused = 0;
 }
 
+void debug_sync_after_launch(const char* file, int line) {
+  fprintf(stderr, "[hb sync] %s:%d ...", file, line);
+  fflush(stderr);
+  const cudaError_t e = cudaDeviceSynchronize();
+  fprintf(stderr, " %s\n", cudaGetErrorString(e));
+}
+
 void context_init(hb_context* c, int device) {
   c->device = device;
   HB_CUDA(cudaSetDevice(device));
@@ -646,8 +655,11 @@ void context_init(hb_context* c, int device) {
   HB_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
   uint64_t thr = UINT64_MAX;
   HB_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
-  HB_CUDA(cudaMalloc(&c->bar, 4 * sizeof(unsigned int)));
-  HB_CUDA(cudaMemset(c->bar, 0, 4 * sizeof(unsigned int)));
+  HB_CUDA(cudaMalloc(&c->bar, 64 * sizeof(unsigned int)));
+  // stream-ordered and waited for: a legacy-stream cudaMemset is not ordered before work on the
+  // non-blocking context stream, and a grid barrier starting from garbage never releases
+  HB_CUDA(cudaMemsetAsync(c->bar, 0, 64 * sizeof(unsigned int), c->stream));
+  HB_CUDA(cudaStreamSynchronize(c->stream));
   HB_CUDA(cudaMallocHost(&c->pinned, 4096));
   for (auto& e : c->ev) HB_CUDA(cudaEventCreate(&e));
   c->bufs.resize(B_COUNT);

@@ -17,6 +17,7 @@
 namespace hb {
 
 __global__ void __launch_bounds__(256) bidiag_kernel(BidiagParams p) {
+  GridSync gbar(p.bar);
   extern __shared__ double bsm[];
   const int G = gridDim.x, g = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -42,7 +43,7 @@ __global__ void __launch_bounds__(256) bidiag_kernel(BidiagParams p) {
     s = warp_sum(s);
     if (tid == 0) p.nslot[g] = s;
   }
-  grid_sync(p.bar);
+  gbar.sync();
 
   for (int64_t i = 0; i < k; ++i) {
     // ---- left reflector from column i ----
@@ -81,14 +82,14 @@ __global__ void __launch_bounds__(256) bidiag_kernel(BidiagParams p) {
         if (lane == 0) p.wslot[(size_t)g * k + q] = s;
       }
     }
-    grid_sync(p.bar);
+    gbar.sync();
     if (i + 1 < k) {
       for (int64_t q = i + 1 + g + (int64_t)warp * G; q < k; q += (int64_t)G * 8) {
         const double s = warp_sum_strided(p.wslot + q, G, k);
         if (lane == 0) p.w[q] = s * tau_u;
       }
     }
-    grid_sync(p.bar);
+    gbar.sync();
     if (i + 1 >= k) break;
     // ---- apply left reflector: M[r, q] -= u_r w_q ----
     for (int64_t q = i + 1 + warp; q < k; q += 8) {
@@ -122,7 +123,7 @@ __global__ void __launch_bounds__(256) bidiag_kernel(BidiagParams p) {
         }
       }
     }
-    grid_sync(p.bar);
+    gbar.sync();
     const double tau_v = p.scal[0];
     // ---- z = M v for own rows r > i, then M[r, q] -= z_r v_q ----
     for (int64_t e = tid; e < 8 * nown * 32; e += 256) zp[e] = 0.0;
@@ -158,7 +159,7 @@ __global__ void __launch_bounds__(256) bidiag_kernel(BidiagParams p) {
     // partial norm of column i+1 (rows > i+1): owned by the warp with q == i+1 (warp 0)
     nrm = warp_sum(nrm);
     if (tid == 0) p.nslot[g] = nrm;
-    grid_sync(p.bar);
+    gbar.sync();
   }
 }
 

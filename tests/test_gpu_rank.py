@@ -69,8 +69,10 @@ def test_certification_sigma_all_bidiag_paths(ctx, oracle, k):
     rng = np.random.default_rng(k)
     q1, _ = np.linalg.qr(rng.standard_normal((k, k)))
     q2, _ = np.linalg.qr(rng.standard_normal((k, k)))
-    s = np.logspace(0, -9, k)
+    s = np.logspace(0, -9.35, k)  # no singular value within 1e-3 (relative) of a threshold
     M = (q1 * s) @ q2.T
+    for t in (1e-12, 1e-6):
+        assert np.min(np.abs(s / t - 1.0)) > 1e-3
     r = rank_dense(ctx, M, [1e-12, 1e-6])
     so = np.linalg.svd(M, compute_uv=False)
     assert [x.rank for x in r] == [oracle.epsilon_rank_from_sigma(so, t).rank for t in (1e-12, 1e-6)]
