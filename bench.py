@@ -89,6 +89,20 @@ def fp64_peak():
         return 37.0, "nominal B200 FP64 (probe file missing)"
 
 
+def ncu_traffic():
+    """DRAM bytes (read + write) of one captured launch of the dominant DMMA GEMM, from the
+    committed ncu --set full summary (profiles/<round>/dgemm_ncu_full.json), or None."""
+    files = sorted(ROOT.glob("profiles/r*/dgemm_ncu_full.json"))
+    if not files:
+        return None, "no ncu --set full capture committed"
+    try:
+        j = json.loads(files[-1].read_text())["roofline_traffic_launch"]
+        return int(j["dram_bytes"]), (f"{files[-1].relative_to(ROOT)}: {j['shape']}, grid {j['grid']}, "
+                                      f"{j['duration_ms']:.3f} ms; algorithmic {j['algorithmic_bytes']} B")
+    except Exception as e:  # noqa: BLE001
+        return None, f"unreadable ncu summary: {e}"
+
+
 def hbm_peak():
     try:
         return float(json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"]), "MEASURED_PEAKS.json"
@@ -328,7 +342,8 @@ def main():
         "roofline": {"bound": "tensor", "kernel": "dgemm_kernel (FP64 DMMA m8n8k4; trailing update, "
                      "sketch, WY and certification QR GEMMs)",
                      "achieved": round(gemm_tf, 3), "peak": peak, "unit": "TFLOP/s",
-                     "frac": round(gemm_tf / peak, 4), "traffic": None, "peak_source": peak_src,
+                     "frac": round(gemm_tf / peak, 4), "traffic": ncu_traffic()[0],
+                     "traffic_source": ncu_traffic()[1], "peak_source": peak_src,
                      "measured": "CUDA events around every DMMA GEMM launch on its stream, timed region",
                      "path": {"alg_tflops": round(path_tf, 3), "frac": round(path_tf / peak, 4),
                               "model": "FLOP_alg = N^2 c_F + 4N^2 p - 4N p^2 + 4/3 p^3 (SURVEY 8d), "

@@ -249,6 +249,217 @@ __global__ void __launch_bounds__(256) sketch_cpqr_kernel(SketchParams p) {
   }
 }
 
+// Shared-memory variant of sketch_cpqr.  Each CTA keeps its ℓ x cpc block of the sketch in
+// shared memory.  Per pivot: every CTA publishes (best norm, index, remaining mass) and the
+// column of its best candidate; after ONE grid barrier all CTAs reduce the slots in the same
+// fixed order (identical decisions everywhere), read the winner's column from its candidate slot,
+// form the Householder vector redundantly, update their own columns and recompute their norms
+// exactly.
+__global__ void __launch_bounds__(kSketchThreads) sketch_cpqr_smem_kernel(SketchParams p) {
+  GridSync gbar(p.bar);
+  constexpr int NW = kSketchThreads / 32;
+  constexpr int RPL = kSketchRows / 32;
+  extern __shared__ double ssm[];
+  const int G = gridDim.x, g = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int ell = p.ell;
+  const int64_t cpc = ceil_div(p.n_tr, G);
+  const int64_t c0 = g * cpc, c1 = min(p.n_tr, c0 + cpc);
+  const int ncol = (int)max((int64_t)0, c1 - c0);
+  double* Ysm = ssm;                          // [cpc][ell]
+  double* nrm_s = ssm + (size_t)cpc * ell;    // [cpc] (-1 = chosen)
+  __shared__ double v[kSketchRows];
+  __shared__ double wbest[NW], wsum[NW];
+  __shared__ int wbi[NW];
+  __shared__ double sh_tau;
+  __shared__ int sh_piv, sh_stop, sh_win;
+
+  double best = -1.0, sum = 0.0;
+  int bi = INT_MAX;
+  for (int q = warp; q < ncol; q += NW) {
+    double s = 0.0;
+#pragma unroll
+    for (int t = 0; t < RPL; ++t) {
+      const int i = lane + 32 * t;
+      double y = 0.0;
+      if (i < ell) y = p.Y[i + (c0 + q) * p.ldy];
+      Ysm[q * ell + i] = y;
+      s += y * y;
+    }
+    s = warp_sum(s);
+    if (lane == 0) nrm_s[q] = s;
+    if (better(s, (int)(c0 + q), best, bi)) { best = s; bi = (int)(c0 + q); }
+    sum += s;
+  }
+  // CTA-level (best, index, mass) -> slot; the best candidate's column -> candidate slot
+  auto publish = [&](int par) {
+    if (lane == 0) { wbest[warp] = best; wbi[warp] = bi; wsum[warp] = sum; }
+    __syncthreads();
+    if (tid == 0) {
+      double b0 = -1.0, s0 = 0.0;
+      int i0 = INT_MAX;
+      for (int w = 0; w < NW; ++w) {
+        if (better(wbest[w], wbi[w], b0, i0)) { b0 = wbest[w]; i0 = wbi[w]; }
+        s0 += wsum[w];
+      }
+      double* sl = p.slots + ((size_t)par * G + g) * 3;
+      sl[0] = b0; sl[1] = (double)i0; sl[2] = s0;
+      sh_win = i0;
+    }
+    __syncthreads();
+    const int w = sh_win;
+    if (w != INT_MAX && tid < ell) p.cand[((size_t)par * G + g) * ell + tid] = Ysm[(w - c0) * ell + tid];
+  };
+  publish(0);
+  gbar.sync();
+
+  int c = 0;
+  for (; c < p.b_req; ++c) {
+    const int par = c & 1;
+    {
+      const double* sl = p.slots + (size_t)par * G * 3;
+      double b0 = -1.0, s0 = 0.0;
+      int i0 = INT_MAX, h0 = -1;
+      for (int h = tid; h < G; h += kSketchThreads) {
+        const double bv = __ldcg(sl + 3 * h);
+        const int iv = (int)__ldcg(sl + 3 * h + 1);
+        if (better(bv, iv, b0, i0)) { b0 = bv; i0 = iv; h0 = h; }
+        s0 += __ldcg(sl + 3 * h + 2);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, b0, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, i0, o);
+        const int oh = __shfl_xor_sync(0xffffffffu, h0, o);
+        if (better(ob, oi, b0, i0)) { b0 = ob; i0 = oi; h0 = oh; }
+      }
+      s0 = warp_sum(s0);
+      if (lane == 0) { wbest[warp] = b0; wbi[warp] = i0; wsum[warp] = s0; v[warp] = (double)h0; }
+      __syncthreads();
+      if (tid == 0) {
+        double bb = -1.0, ss = 0.0;
+        int ii = INT_MAX, hh = -1;
+        for (int w = 0; w < NW; ++w) {
+          if (better(wbest[w], wbi[w], bb, ii)) { bb = wbest[w]; ii = wbi[w]; hh = (int)v[w]; }
+          ss += wsum[w];
+        }
+        const double est = c < ell ? ss / (double)(ell - c) : 0.0;
+        if (g == 0) p.out_est[c] = est;
+        int stop = 0;
+        if (!(bb > 0.0) || c >= ell) stop = 1;
+        else if (c >= p.b_min && (c % 8) == 0 && est <= p.stop_fro2) stop = 1;
+        sh_stop = stop;
+        sh_piv = ii;
+        sh_win = hh;
+      }
+      __syncthreads();
+    }
+    if (sh_stop) break;
+    const int piv = sh_piv;
+    // Householder vector of the winner's column (rows c..ell-1), redundantly in every CTA
+    if (warp == 0) {
+      const double* col = p.cand + ((size_t)par * G + sh_win) * ell;
+      double yv[RPL];
+      double s = 0.0;
+#pragma unroll
+      for (int t = 0; t < RPL; ++t) {
+        const int i = lane + 32 * t;
+        yv[t] = i < ell ? __ldcg(col + i) : 0.0;
+        if (i > c && i < ell) s += yv[t] * yv[t];
+      }
+      s = warp_sum(s);
+      const int tc = c >> 5;
+      const double yc = tc == 0 ? yv[0] : (tc == 1 ? yv[1] : (tc == 2 ? yv[2] : yv[3]));
+      const double alpha = __shfl_sync(0xffffffffu, yc, c & 31);
+      double tau = 0.0, scal = 0.0, beta = alpha;
+      if (s > 0.0) {
+        beta = -copysign(sqrt(alpha * alpha + s), alpha);
+        tau = (beta - alpha) / beta;
+        scal = 1.0 / (alpha - beta);
+      }
+#pragma unroll
+      for (int t = 0; t < RPL; ++t) {
+        const int i = lane + 32 * t;
+        if (i < kSketchRows) v[i] = i < c ? 0.0 : (i == c ? 1.0 : (i < ell ? yv[t] * scal : 0.0));
+      }
+      if (lane == 0) {
+        sh_tau = tau;
+        if (g == 0) { p.piv[c] = piv; p.rdiag[c] = fabs(beta); }
+      }
+    }
+    __syncthreads();
+    const double tau = sh_tau;
+    double vr[RPL];
+#pragma unroll
+    for (int t = 0; t < RPL; ++t) vr[t] = v[lane + 32 * t];
+    if (piv >= c0 && piv < c1 && tid == 0) nrm_s[piv - c0] = -1.0;
+    __syncthreads();
+    best = -1.0; sum = 0.0; bi = INT_MAX;
+    for (int qa = warp; qa < ncol; qa += 2 * NW) {
+      const int qb = qa + NW;
+      const bool va = nrm_s[qa] >= 0.0;
+      const bool vb = qb < ncol && nrm_s[qb] >= 0.0;
+      double* ca = Ysm + (size_t)qa * ell;
+      double* cb = Ysm + (size_t)qb * ell;
+      double ya[RPL], yb[RPL];
+#pragma unroll
+      for (int t = 0; t < RPL; ++t) {
+        const int i = lane + 32 * t;
+        ya[t] = va ? ca[i] : 0.0;
+        yb[t] = vb ? cb[i] : 0.0;
+      }
+      double wa = 0.0, wb = 0.0;
+#pragma unroll
+      for (int t = 0; t < RPL; ++t) { wa = fma(vr[t], ya[t], wa); wb = fma(vr[t], yb[t], wb); }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        wa += __shfl_xor_sync(0xffffffffu, wa, o);
+        wb += __shfl_xor_sync(0xffffffffu, wb, o);
+      }
+      wa *= tau; wb *= tau;
+      double sa = 0.0, sb = 0.0;
+#pragma unroll
+      for (int t = 0; t < RPL; ++t) {
+        const int i = lane + 32 * t;
+        const double xa = fma(-wa, vr[t], ya[t]), xb = fma(-wb, vr[t], yb[t]);
+        if (va) ca[i] = xa;
+        if (vb) cb[i] = xb;
+        if (i > c) { sa = fma(xa, xa, sa); sb = fma(xb, xb, sb); }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        sa += __shfl_xor_sync(0xffffffffu, sa, o);
+        sb += __shfl_xor_sync(0xffffffffu, sb, o);
+      }
+      if (va) {
+        if (lane == 0) nrm_s[qa] = sa;
+        if (better(sa, (int)(c0 + qa), best, bi)) { best = sa; bi = (int)(c0 + qa); }
+        sum += sa;
+      }
+      if (vb) {
+        if (lane == 0) nrm_s[qb] = sb;
+        if (better(sb, (int)(c0 + qb), best, bi)) { best = sb; bi = (int)(c0 + qb); }
+        sum += sb;
+      }
+    }
+    __syncthreads();
+    publish(par ^ 1);
+    gbar.sync();
+  }
+  if (g == 0 && tid == 0) {
+    int pos[kBlockMax];
+    for (int i = 0; i < c; ++i) pos[i] = p.piv[i];
+    for (int i = 0; i < c; ++i) {
+      const int src = pos[i];
+      p.swaps[i] = src;
+      if (src != i)
+        for (int t = i + 1; t < c; ++t)
+          if (pos[t] == i) pos[t] = src;
+    }
+    *p.out_b = c;
+  }
+}
+
 // ------------------------------------------------------------------------------------------
 // permute: apply the swap list to A (all m rows), Y (ℓ rows) and perm (one row).
 // ------------------------------------------------------------------------------------------

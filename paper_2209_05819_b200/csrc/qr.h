@@ -21,6 +21,7 @@ struct SketchParams {
   double* rdiag;    // [b_req] |R_cc| of the sketch
   double* out_est;  // [b_req + 1] sketch estimate of ||A22||_F^2 before step c
   int* out_b;       // pivots chosen
+  double* cand;     // [2][G][ell] best candidate column per CTA (shared-memory variant)
   GridBarrier bar;
 };
 
@@ -69,6 +70,10 @@ struct BidiagParams {
 };
 
 __global__ void sketch_cpqr_kernel(SketchParams p);
+// Shared-memory-resident variant (sketch columns of a CTA fit in ~200 KB): one barrier per pivot,
+// the winner's column travels through a per-CTA candidate slot instead of the global sketch.
+constexpr int kSketchThreads = 512;
+__global__ void sketch_cpqr_smem_kernel(SketchParams p);
 __global__ void permute_kernel(double* A, int64_t lda, int64_t m, double* Y, int64_t ldy, int ell,
                                int64_t* perm, int64_t j, const int* swaps, const int* bptr);
 __global__ void panel_qr_kernel(PanelParams p);

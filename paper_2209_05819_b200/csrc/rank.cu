@@ -360,6 +360,7 @@ void rank_matrix_inplace(hb_context* c, double* A, int64_t m, int64_t n, int64_t
   int64_t* perm = ws<int64_t>(c, B_PERM, (size_t)n);
   double* scal = ws<double>(c, B_FROSUM, 8);  // [0] fro², [1] σ̂₁
   double* sk_slots = ws<double>(c, B_SCAL, (size_t)c->num_sms * 12 + 16);  // [2][G <= 2 SMs][3]
+  double* sk_cand = ws<double>(c, B_SKCAND, (size_t)2 * c->num_sms * kSketchRows);  // [2][G][ℓ]
   iota_kernel<<<(unsigned)ceil_div(std::max<int64_t>(n, 1), 256), 256, 0, c->stream>>>(perm, n);
   HB_LAUNCH_CHECK();
 
@@ -372,6 +373,24 @@ void rank_matrix_inplace(hb_context* c, double* A, int64_t m, int64_t n, int64_t
   int64_t j = 0;
   int b = std::min(32, c->block_max);
   double sigma1_est = 0.0, delta = 0.0, fro_at_sketch = INFINITY;
+  if (kmax > 0 && c->block_max >= 64) {
+    // σ̂₁ for the first block's stopping test from the sketch: ‖Ω A‖₂ ≈ sqrt(ℓ)·σ₁ (half of it,
+    // for margin).  Not a bound — an overestimate can only stop a block early, which the exact
+    // residual test after the update (and, at worst, a re-certification round) catches — but
+    // it lets the first block run at the full width instead of 32 -> 64 -> 120 ramp-up blocks.
+    Phase ph(c, HB_PH_SIGMA1);
+    PowerParams pw{};
+    pw.R = Y; pw.ld = ell; pw.b = std::min(ell, kBlockMax); pw.n = n; pw.iters = 4; pw.mask = 0;
+    pw.slots = ws<double>(c, B_SIG1, (size_t)2 * c->num_sms * (kBlockMax + 1));
+    pw.out = scal + 1; pw.bar = barrier(c);
+    coop(power_sigma1_kernel, clampi(ceil_div(n, 256), 1, c->coop_sms), 0, st, pw);
+    double sy = 0.0;
+    sync_to_host(c, scal + 1, &sy, sizeof(double));
+    if (sy > 0.0 && std::isfinite(sy)) {
+      sigma1_est = 0.5 * sy / std::sqrt((double)pw.b);
+      b = c->block_max;
+    }
+  }
   bool first = true;
   int zero_retries = 0;
   // Factor until ||A22||_F <= eta·tol·σ̂₁, certify, and only if some bracket stays open
@@ -397,8 +416,17 @@ void rank_matrix_inplace(hb_context* c, double* A, int64_t m, int64_t n, int64_t
       sp.out_b = beff; sp.bar = barrier(c);
       {
         Phase ph(c, HB_PH_PIVOT);
-        const int Gs = clampi(ceil_div(n_tr, 64), 1, 2 * c->coop_sms);
-        coop(sketch_cpqr_kernel, Gs, (size_t)ceil_div(n_tr, Gs) * sizeof(double), st, sp);
+        // shared-memory variant when every CTA's ℓ x cpc sketch block fits (~200 KB)
+        const int Gm = clampi(ceil_div(n_tr, 64), 1, c->coop_sms);
+        const int64_t cpcm = ceil_div(n_tr, Gm);
+        const size_t smem_m = ((size_t)cpcm * ell + cpcm) * sizeof(double);
+        if (ell == kSketchRows && smem_m <= 200 * 1024) {
+          sp.cand = sk_cand;
+          coop(sketch_cpqr_smem_kernel, Gm, smem_m, st, sp, kSketchThreads);
+        } else {
+          const int Gs = clampi(ceil_div(n_tr, 64), 1, 2 * c->coop_sms);
+          coop(sketch_cpqr_kernel, Gs, (size_t)ceil_div(n_tr, Gs) * sizeof(double), st, sp);
+        }
       }
       int bh = 0;
       sync_to_host(c, beff, &bh, sizeof(int));
@@ -441,7 +469,7 @@ void rank_matrix_inplace(hb_context* c, double* A, int64_t m, int64_t n, int64_t
       if (first) {
         Phase ph(c, HB_PH_SIGMA1);
         PowerParams pw{};
-        pw.R = A; pw.ld = lda; pw.b = bh; pw.n = n; pw.iters = 12; pw.mask = 1;  // a lower bound suffices
+        pw.R = A; pw.ld = lda; pw.b = bh; pw.n = n; pw.iters = 5; pw.mask = 1;  // any iterate is a lower bound
         pw.slots = ws<double>(c, B_SIG1, (size_t)2 * c->num_sms * (kBlockMax + 1));
         pw.out = scal + 1; pw.bar = barrier(c);
         coop(power_sigma1_kernel, clampi(ceil_div(n, 256), 1, c->coop_sms), 0, st, pw);
