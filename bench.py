@@ -196,7 +196,7 @@ def main():
     ap.add_argument("--workload", default="c1", choices=["c0", "c1", "c2", "c3", "sweep"],
                     help="BASELINE.json configs[0..3] (c0..c3) or the full configs[4] sweep")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-sample-max-n", type=int, default=2000,
+    ap.add_argument("--cpu-sample-max-n", type=int, default=4000,
                     help="CPU baseline sample: the workload's problems with N <= this")
     ap.add_argument("--details", default="", help="write per-problem results/stats JSON here")
     args = ap.parse_args()
