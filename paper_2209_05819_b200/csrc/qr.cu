@@ -838,6 +838,40 @@ __global__ void transpose_upper_kernel(const double* __restrict__ A, int64_t lda
   }
 }
 
+// λ_max lower bound of the symmetric positive semidefinite b x b Gram matrix G (ld b) by power
+// iteration in one CTA: every Rayleigh quotient xᵀGx / xᵀx is <= λ_max, so sqrt of the largest
+// one seen is a lower bound on σ₁ of the matrix whose Gram G is (up to rounding).
+__global__ void __launch_bounds__(256) gram_sigma1_kernel(const double* __restrict__ G, int b, int iters,
+                                                          double* __restrict__ out) {
+  extern __shared__ double gs[];  // b x b
+  __shared__ double x[kSketchRows], y[kSketchRows], red[32];
+  const int tid = threadIdx.x;
+  for (int e = tid; e < b * b; e += blockDim.x) gs[e] = G[e];
+  for (int i = tid; i < b; i += blockDim.x) x[i] = 1.0;
+  __syncthreads();
+  double best = 0.0;
+  for (int it = 0; it < iters; ++it) {
+    double xx = 0.0, xy = 0.0;
+    for (int i = tid; i < b; i += blockDim.x) {
+      double s = 0.0;
+      for (int j = 0; j < b; ++j) s = fma(gs[i + j * b], x[j], s);  // G symmetric: row i = column i
+      y[i] = s;
+      xx += x[i] * x[i];
+      xy += x[i] * s;
+    }
+    xx = block_sum(xx, red);
+    xy = block_sum(xy, red);
+    if (xx > 0.0) best = fmax(best, xy / xx);
+    double yy = 0.0;
+    for (int i = tid; i < b; i += blockDim.x) yy += y[i] * y[i];
+    yy = block_sum(yy, red);
+    const double sc = yy > 0.0 ? 1.0 / sqrt(yy) : 0.0;
+    for (int i = tid; i < b; i += blockDim.x) x[i] = y[i] * sc;
+    __syncthreads();
+  }
+  if (tid == 0) *out = sqrt(fmax(best, 0.0));
+}
+
 // C (k x k) = upper triangle of B[0:k, 0:k].
 __global__ void copy_upper_kernel(const double* __restrict__ B, int64_t ldb, int64_t k,
                                   double* __restrict__ C, int64_t ldc) {

@@ -84,6 +84,7 @@ __global__ void sketch_trsm_kernel(const double* Y1, int64_t ldy, int ell, const
                                    int64_t ldr, int b, double* Z, int64_t ldz);
 __global__ void power_sigma1_kernel(PowerParams p);
 __global__ void sum_kernel(const double* parts, int64_t n, double* out);
+__global__ void gram_sigma1_kernel(const double* G, int b, int iters, double* out);
 __global__ void transpose_upper_kernel(const double* A, int64_t lda, int64_t k, int64_t n, double* B,
                                        int64_t ldb);
 __global__ void copy_upper_kernel(const double* B, int64_t ldb, int64_t k, double* C, int64_t ldc);
@@ -116,7 +117,8 @@ int bidiag_cluster_size(int k);
 void launch_bidiag_cluster(const double* Mk, int64_t ldm, int k, double* d, double* e, int G,
                            cudaStream_t st);
 __global__ void sigma_queries_kernel(const double* d, const double* e, int64_t k,
-                                     const SigmaQuery* q, int nq, SigmaAnswer* out);
+                                     const SigmaQuery* q, int nq, SigmaAnswer* out,
+                                     double* tg_glob, int tg_smem);
 __global__ void sigma_all_kernel(const double* d, const double* e, int64_t k, double sigma_max,
                                  double* out);
 

@@ -69,6 +69,31 @@ void build_T(hb_context* c, const double* V, int64_t ldv, int64_t mp, int b, con
   HB_LAUNCH_CHECK();
 }
 
+// Lower bound on σ₁ of the rows x n matrix X (ld): Gram G = X Xᵀ by one DMMA GEMM on the
+// transposed copy, then a one-CTA power iteration on G (rows <= 128).  upper_trap: X holds the
+// first rows of R (entries below the diagonal of the leading block are Householder vectors and
+// count as zero).  Replaces a grid-wide power iteration whose per-column dot products were
+// latency-serialised (~200 µs per call).
+double sigma1_lower_bound(hb_context* c, const double* X, int64_t ld, int rows, int64_t n,
+                          bool upper_trap, double* dev_out) {
+  cudaStream_t st = c->stream;
+  double* Xt = ws<double>(c, B_PX, (size_t)n * rows);
+  dim3 tb(32, 8), tg((unsigned)ceil_div(n, 32), (unsigned)ceil_div(rows, 32));
+  if (upper_trap) transpose_upper_kernel<<<tg, tb, 0, st>>>(X, ld, rows, n, Xt, n);
+  else transpose_kernel<<<tg, tb, 0, st>>>(X, ld, rows, n, Xt, n);
+  HB_LAUNCH_CHECK();
+  double* G = ws<double>(c, B_PY, (size_t)kSketchRows * kSketchRows);
+  GemmArgs g{};
+  g.M = rows; g.N = rows; g.K = n; g.alpha = 1.0; g.A = Xt; g.lda = n; g.transA = true;
+  g.B = Xt; g.ldb = n; g.beta = 0.0; g.C = G; g.ldc = rows;
+  Gemm{c}(g);
+  const size_t smem = (size_t)rows * rows * sizeof(double);
+  ensure_dyn_smem((const void*)gram_sigma1_kernel, smem);
+  gram_sigma1_kernel<<<1, 256, smem, st>>>(G, rows, 40, dev_out);
+  HB_LAUNCH_CHECK();
+  return 0.0;
+}
+
 // Householder QR of the mp x b panel at P (ld): R and V in place, explicit V (ld ldv), τ, and T
 // (ld b) of Q = I − V T Vᵀ.  The shared-memory-resident kernel handles up to ~200 KB of panel
 // rows per CTA; wider panels are factored as column sub-panels joined by a block-reflector
@@ -379,15 +404,11 @@ void rank_matrix_inplace(hb_context* c, double* A, int64_t m, int64_t n, int64_t
     // residual test after the update (and, at worst, a re-certification round) catches — but
     // it lets the first block run at the full width instead of 32 -> 64 -> 120 ramp-up blocks.
     Phase ph(c, HB_PH_SIGMA1);
-    PowerParams pw{};
-    pw.R = Y; pw.ld = ell; pw.b = std::min(ell, kBlockMax); pw.n = n; pw.iters = 4; pw.mask = 0;
-    pw.slots = ws<double>(c, B_SIG1, (size_t)2 * c->num_sms * (kBlockMax + 1));
-    pw.out = scal + 1; pw.bar = barrier(c);
-    coop(power_sigma1_kernel, clampi(ceil_div(n, 256), 1, c->coop_sms), 0, st, pw);
+    sigma1_lower_bound(c, Y, ell, ell, n, false, scal + 1);
     double sy = 0.0;
     sync_to_host(c, scal + 1, &sy, sizeof(double));
     if (sy > 0.0 && std::isfinite(sy)) {
-      sigma1_est = 0.5 * sy / std::sqrt((double)pw.b);
+      sigma1_est = 0.5 * sy / std::sqrt((double)ell);
       b = c->block_max;
     }
   }
@@ -468,11 +489,7 @@ void rank_matrix_inplace(hb_context* c, double* A, int64_t m, int64_t n, int64_t
       ph_up.close();
       if (first) {
         Phase ph(c, HB_PH_SIGMA1);
-        PowerParams pw{};
-        pw.R = A; pw.ld = lda; pw.b = bh; pw.n = n; pw.iters = 5; pw.mask = 1;  // any iterate is a lower bound
-        pw.slots = ws<double>(c, B_SIG1, (size_t)2 * c->num_sms * (kBlockMax + 1));
-        pw.out = scal + 1; pw.bar = barrier(c);
-        coop(power_sigma1_kernel, clampi(ceil_div(n, 256), 1, c->coop_sms), 0, st, pw);
+        sigma1_lower_bound(c, A, lda, bh, n, true, scal + 1);
       }
       if (n2 > 0) {
         Phase ph(c, HB_PH_DOWNDATE);
@@ -581,7 +598,11 @@ void rank_matrix_inplace(hb_context* c, double* A, int64_t m, int64_t n, int64_t
       SigmaQuery* dq = ws<SigmaQuery>(c, B_QUERY, 2 * HB_MAX_TOLS);
       SigmaAnswer* da = ws<SigmaAnswer>(c, B_ANSWER, 2 * HB_MAX_TOLS);
       HB_CUDA(cudaMemcpyAsync(dq, hq, sizeof(SigmaQuery) * nq, cudaMemcpyHostToDevice, st));
-      sigma_queries_kernel<<<1, 32 * 4 * HB_MAX_TOLS, 0, st>>>(d, e, k, dq, nq, da);
+      const size_t tg_bytes = (size_t)(2 * k) * sizeof(double);
+      const int tg_smem = tg_bytes <= 200 * 1024 ? 1 : 0;
+      double* tg_glob = tg_smem ? nullptr : ws<double>(c, B_TG, (size_t)2 * k);
+      if (tg_smem) ensure_dyn_smem((const void*)sigma_queries_kernel, tg_bytes);
+      sigma_queries_kernel<<<1, 512, tg_smem ? tg_bytes : 0, st>>>(d, e, k, dq, nq, da, tg_glob, tg_smem);
       HB_LAUNCH_CHECK();
       sync_to_host(c, da, ans, sizeof(SigmaAnswer) * nq);
     }

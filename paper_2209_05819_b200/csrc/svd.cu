@@ -226,44 +226,141 @@ __device__ double tgk_bounds(const double* d, const double* e, int64_t k, double
   return ub * (1.0 + 1e-14) + 1e-300;
 }
 
-__global__ void sigma_queries_kernel(const double* __restrict__ d, const double* __restrict__ e,
-                                     int64_t k, const SigmaQuery* __restrict__ q, int nq,
-                                     SigmaAnswer* __restrict__ out) {
-  __shared__ double sh_s1, sh_pivmin, sh_ub;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (warp == 0) {
-    double pivmin = 0.0, ub = 0.0;
-    if (lane == 0) ub = tgk_bounds(d, e, k, &pivmin);
-    ub = __shfl_sync(0xffffffffu, ub, 0);
-    pivmin = __shfl_sync(0xffffffffu, pivmin, 0);
-    const double s1 = k > 0 ? kth_largest(d, e, k, 1, 0.0, ub, pivmin) : 0.0;
-    if (lane == 0) { sh_s1 = s1; sh_pivmin = pivmin; sh_ub = ub; }
+// ---- block-wide Sturm-count multisection -------------------------------------------------
+// count on the squared TGK off-diagonals tg[u] = a_u², u = 0..2k-2 (a = d0, e0, d1, e1, ...):
+// the same recurrence and rounding as count_less above.
+__device__ __forceinline__ int64_t count_less_sq(const double* __restrict__ tg, int64_t k, double x,
+                                                 double pivmin) {
+  double q = -x;
+  int64_t neg = q < 0.0;
+  const int64_t n2 = 2 * k - 1;
+  for (int64_t u = 0; u < n2; ++u) {
+    if (fabs(q) < pivmin) q = -pivmin;
+    q = -x - tg[u] / q;
+    neg += q < 0.0;
   }
-  __syncthreads();
-  const double s1 = sh_s1, pivmin = sh_pivmin;
-  // two warps per query: one bisects σ_p, the other σ_{p+1} (both need p: one count each)
-  for (int task = warp; task < 2 * nq; task += blockDim.x / 32) {
-    const int qi = task >> 1, half = task & 1;
-    const double thr = q[qi].tol * s1;
-    const double xp = nextafter(thr, 1e308);
-    const int64_t p = k - count_less(d, e, k, xp, pivmin);
-    if (half == 0) {
-      const double thr2 = thr * thr - q[qi].delta * q[qi].delta;
-      const double thr_hi = thr2 > 0.0 ? sqrt(thr2) : 0.0;
-      const int64_t phi = thr_hi > 0.0 ? k - count_less(d, e, k, nextafter(thr_hi, 1e308), pivmin) : k;
-      double sp = 0.0;
-      if (!q[qi].counts_only && p >= 1) sp = kth_largest(d, e, k, p, thr, sh_ub, pivmin, 1e-13);
-      if (lane == 0) {
-        out[qi].sigma1 = s1;
-        out[qi].sigma_p = sp;
-        out[qi].rank_lo = (int)p;
-        out[qi].rank_hi = (int)phi;
-      }
-    } else {
-      double sp1 = 0.0;
-      if (!q[qi].counts_only && p + 1 <= k) sp1 = kth_largest(d, e, k, p + 1, 0.0, xp, pivmin, 1e-13);
-      if (lane == 0) out[qi].sigma_p1 = sp1;
+  return neg - k;
+}
+
+__device__ __forceinline__ void group_bar(int id, int nthreads) {
+  if (id == 0) __syncthreads();
+  else asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// j-th largest singular value by (32·nw)-way multisection shared by the nw warps of a group
+// (warp gw of the group, named barrier bar_id; bar_id < 0: single warp, no barrier).  Every
+// thread of the group ends with the same bracket (identical masks and arithmetic).
+__device__ double kth_group(const double* tg, int64_t k, int64_t j, double lo, double hi,
+                            double pivmin, double rel, int gw, int nw, unsigned* masks, int bar_id) {
+  const int lane = threadIdx.x & 31;
+  const int npts = 32 * nw;
+  const double inv = 1.0 / (double)(npts + 1);
+  const int64_t need = k - j + 1;
+  int par = 0;
+  auto first_true = [&](bool pred) {
+    const unsigned m = __ballot_sync(0xffffffffu, pred);
+    if (nw == 1) return m ? __ffs(m) - 1 : 32;
+    if (lane == 0) masks[par * nw + gw] = m;
+    group_bar(bar_id, 32 * nw);
+    int f = npts;
+    for (int w = 0; w < nw; ++w) {
+      const unsigned mm = masks[par * nw + w];
+      if (mm) { f = 32 * w + __ffs(mm) - 1; break; }
     }
+    par ^= 1;
+    return f;
+  };
+  if (!(lo > 0.0)) lo = hi * 1e-300;
+  for (int it = 0; it < 12 && hi > 4.0 * lo; ++it) {
+    const double lr = log(hi / lo);
+    const int idx = 32 * gw + lane;
+    const double x = lo * exp(lr * (double)(idx + 1) * inv);
+    const int f = first_true(count_less_sq(tg, k, x, pivmin) >= need);
+    const double nlo = f == 0 ? lo : lo * exp(lr * (double)f * inv);
+    const double nhi = f == npts ? hi : lo * exp(lr * (double)(f + 1) * inv);
+    lo = nlo; hi = nhi;
+  }
+  for (int it = 0; it < 40; ++it) {
+    if (!(hi - lo > rel * hi)) break;
+    const int idx = 32 * gw + lane;
+    const double w = hi - lo;
+    const double x = lo + w * (double)(idx + 1) * inv;
+    const int f = first_true(count_less_sq(tg, k, x, pivmin) >= need);
+    const double nlo = f == 0 ? lo : lo + w * (double)f * inv;
+    const double nhi = f == npts ? hi : lo + w * (double)(f + 1) * inv;
+    lo = nlo; hi = nhi;
+  }
+  return 0.5 * (lo + hi);
+}
+
+// σ₁ and, per query, rank_lo / rank_hi counts and σ_p, σ_{p+1} — all 16 warps of the block:
+// σ₁ by a 512-point multisection from the bracket [max |entry|, Gershgorin bound] (no geometric
+// phase), then 2·nq bisections with 16/(2·nq) warps each.  The squared off-diagonals live in
+// shared memory when they fit (tg_smem), else in the global scratch tg_glob.
+__global__ void __launch_bounds__(512) sigma_queries_kernel(const double* __restrict__ d,
+                                                            const double* __restrict__ e, int64_t k,
+                                                            const SigmaQuery* __restrict__ q, int nq,
+                                                            SigmaAnswer* __restrict__ out,
+                                                            double* __restrict__ tg_glob, int tg_smem) {
+  extern __shared__ double tgs[];
+  __shared__ unsigned masks[2 * 16];
+  __shared__ unsigned gmasks[8][2 * 8];
+  __shared__ double redmax[2][16];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double* tg = tg_smem ? tgs : tg_glob;
+  const int64_t n2 = 2 * k - 1;
+  double amax = 0.0, ub = 0.0;
+  for (int64_t u = tid; u < n2; u += blockDim.x) {
+    const double a = fabs((u & 1) ? e[(u - 1) >> 1] : d[u >> 1]);
+    tg[u] = a * a;
+    const double an = u + 1 < n2 ? fabs(((u + 1) & 1) ? e[u >> 1] : d[(u + 1) >> 1]) : 0.0;
+    amax = fmax(amax, a);
+    ub = fmax(ub, a + an);
+    if (u == 0) ub = fmax(ub, a);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+    ub = fmax(ub, __shfl_xor_sync(0xffffffffu, ub, o));
+  }
+  if (lane == 0) { redmax[0][warp] = amax; redmax[1][warp] = ub; }
+  __syncthreads();
+  amax = 0.0; ub = 0.0;
+  for (int w = 0; w < 16; ++w) { amax = fmax(amax, redmax[0][w]); ub = fmax(ub, redmax[1][w]); }
+  const double pivmin = 1e-290 * fmax(1.0, amax * amax);
+  ub = ub * (1.0 + 1e-14) + 1e-300;
+  if (k <= 0) {
+    if (tid < nq) { out[tid].sigma1 = 0.0; out[tid].sigma_p = 0.0; out[tid].sigma_p1 = 0.0; out[tid].rank_lo = 0; out[tid].rank_hi = 0; }
+    return;
+  }
+  // σ₁: the largest entry is a lower bound, the Gershgorin bound an upper one
+  const double s1 = kth_group(tg, k, 1, amax * (1.0 - 1e-15), ub, pivmin, 4e-16, warp, 16, masks, 0);
+  // queries: 2·nq tasks, W warps each
+  const int ntask = 2 * nq;
+  int W = 16 / ntask;
+  W = W >= 8 ? 8 : (W >= 4 ? 4 : (W >= 2 ? 2 : 1));
+  const int task = warp / W, gw = warp % W;
+  if (task >= ntask) return;
+  const int qi = task >> 1, half = task & 1;
+  const double thr = q[qi].tol * s1;
+  const double xp = nextafter(thr, 1e308);
+  const int64_t p = k - count_less_sq(tg, k, xp, pivmin);
+  const int bar_id = W > 1 ? 1 + task : -1;
+  if (half == 0) {
+    const double thr2 = thr * thr - q[qi].delta * q[qi].delta;
+    const double thr_hi = thr2 > 0.0 ? sqrt(thr2) : 0.0;
+    const int64_t phi = thr_hi > 0.0 ? k - count_less_sq(tg, k, nextafter(thr_hi, 1e308), pivmin) : k;
+    double sp = 0.0;
+    if (!q[qi].counts_only && p >= 1) sp = kth_group(tg, k, p, thr, ub, pivmin, 1e-13, gw, W, gmasks[task], bar_id);
+    if (gw == 0 && lane == 0) {
+      out[qi].sigma1 = s1;
+      out[qi].sigma_p = sp;
+      out[qi].rank_lo = (int)p;
+      out[qi].rank_hi = (int)phi;
+    }
+  } else {
+    double sp1 = 0.0;
+    if (!q[qi].counts_only && p + 1 <= k) sp1 = kth_group(tg, k, p + 1, 0.0, xp, pivmin, 1e-13, gw, W, gmasks[task], bar_id);
+    if (gw == 0 && lane == 0) out[qi].sigma_p1 = sp1;
   }
 }
 

@@ -16,6 +16,10 @@ SHAPES = [  # (transA, M, N, K, beta): name
     ((0, 16384, 16384, 32, 1.0), "band-reduction update (K=32)"),
     ((1, 64, 32768, 32768, 0.0), "W = V^T A2 (TN reduce, M=b=64)"),
     ((0, 32768, 32768, 64, 1.0), "trailing update (K=b=64)"),
+    ((0, 32768, 32768, 240, 1.0), "trailing update (K=2b=240)"),
+    ((1, 240, 32768, 32768, 0.0), "W = V^T A2 (TN reduce, M=2b=240)"),
+    ((0, 65536, 65536, 120, 1.0), "trailing update N=65536 (K=120)"),
+    ((0, 65536, 65536, 240, 1.0), "trailing update N=65536 (K=240)"),
 ]
 ctx = hb.Context(0)
 s = torch.cuda.ExternalStream(ctx.stream)
