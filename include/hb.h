@@ -17,6 +17,10 @@
  *   hb_rank_matrix         <- SPEC epsilon_rank(matrix, epsilon)
  *   hb_rank                <- SPEC pair_geometry -> assemble_dense -> epsilon_rank
  *   hb_sweep               <- SPEC rank_table + parallel_for        SPEC.md:570-578, parallel.hpp:12-29
+ *   hb_block               <- hodlr::BlockSpec index ranges         aca.hpp:16-28
+ *   hb_aca_factor          <- hodlr::ACAFactor                      aca.hpp:50-62
+ *   hb_aca_compress        <- hodlr::compress (aca_sweep)           aca.hpp:72-198
+ *   hb_aca_apply           <- hodlr::apply                          aca.hpp:202-213
  * Error mapping (reference exceptions -> status):
  *   std::invalid_argument -> HB_EINVAL   (kernel.hpp:171-173, geometry.hpp:22)
  *   std::length_error     -> HB_ECAP     (kernel.hpp:174-175, entry cap)
@@ -204,6 +208,41 @@ void hb_sweep_release(void);
 
 /* LPT assignment used by hb_sweep / multi-process sweeps: owner[i] in [0, nparts). */
 hb_status hb_partition(const hb_problem* probs, int64_t n, int32_t nparts, int32_t* owner);
+
+/* ---- ACA: the reference's own rank(ε) factorisation (aca.hpp:16-213) --------------------------
+ * Partially pivoted ACA of the kernel block K(I, J), entries recomputed on the fly on the device;
+ * pivot rules, stopping test ||u_r|| ||v_r|| <= ε ||A_r||_F, degenerate-pivot re-sweep at ε/10
+ * and truncation exactly as aca.hpp.  Errors: ε <= 0, max_rank < 1 or an empty block ->
+ * HB_EINVAL (aca.hpp:172-175); block outside the point sets -> HB_EINVAL; r == 0 on a singular
+ * kernel without a diagonal value -> HB_ESINGULAR. */
+/* BlockSpec: rows [row_begin, row_begin + rows) of the targets x columns [col_begin, col_begin +
+ * cols) of the sources (aca.hpp:26-28). */
+typedef struct {
+  int64_t row_begin;
+  int64_t rows;
+  int64_t col_begin;
+  int64_t cols;
+} hb_block;
+typedef struct hb_aca_factor hb_aca_factor; /* opaque ACAFactor; L / U stay on the device */
+
+/* compress every block of `blocks` (one factor each in out[0..nblocks)); blocks that fit one CTA
+ * run batched in one launch, larger ones on a cooperative group of CTAs.  Point sets are device
+ * SoA arrays (nt targets, ns sources, dimension d). */
+hb_status hb_aca_compress(hb_context* ctx, const hb_kernel* kernel, const double* d_tgt_soa,
+                          int64_t nt, const double* d_src_soa, int64_t ns, int32_t d,
+                          const hb_block* blocks, int64_t nblocks, double eps, int64_t max_rank,
+                          hb_aca_factor** out);
+/* rank, tolerance_met and ACAFactor::memory_bytes (aca.hpp:58-61); any pointer may be NULL. */
+hb_status hb_aca_factor_info(const hb_aca_factor* f, int32_t* rank, int32_t* tolerance_met,
+                             int64_t* memory_bytes);
+/* Host copies: sigma / tau (rank global ids), L / U (rank x rank column-major); NULL skips. */
+hb_status hb_aca_factor_copy(const hb_aca_factor* f, int64_t* sigma, int64_t* tau, double* L,
+                             double* U);
+/* b = K(I, τ) U⁻¹ L⁻¹ K(σ, J) q with device vectors q (block cols) and b (block rows). */
+hb_status hb_aca_apply(hb_context* ctx, const hb_aca_factor* f, const hb_kernel* kernel,
+                       const double* d_tgt_soa, int64_t nt, const double* d_src_soa, int64_t ns,
+                       int32_t d, const hb_block* block, const double* d_q, double* d_b);
+void hb_aca_factor_destroy(hb_aca_factor* f);
 
 /* Deterministic per-problem seed = hash(base, d, d', N). */
 uint64_t hb_problem_seed(uint64_t base, int32_t d, int32_t d_prime, int64_t n);

@@ -16,6 +16,7 @@
  *     sequential sum of squares)            sum; pinned here with -ffp-contract=off, IEEE sqrt)
  *   HyperCube{lower, side}                  geometry.hpp:15-64
  *   parallel_for static chunking            parallel.hpp:12-29
+ *   BlockSpec / aca_sweep / compress / apply aca.hpp:16-213
  * The seeded point generator is this project's own definition (BASELINE.json configs say
  * "uniform fp64 points per cube from seed"); the grid modes follow SURVEY.md A.1.
  */
@@ -52,6 +53,20 @@ int hbo_assemble(int kernel_id, int has_diag, double diag, const double* x_soa, 
                  int64_t entry_cap);
 
 uint64_t hbo_splitmix64(uint64_t x);
+
+/* bessel::j2 / bessel::y2 (bessel.hpp:129-144), __float128 series / long double asymptotics. */
+double hbo_j2(double x);
+double hbo_y2(double x);
+
+/* hodlr::compress (aca.hpp:171-198) of the block K(rb:rb+rows, cb:cb+cols) of the kernel over
+ * target / source point sets (SoA, nt / ns points), then optionally hodlr::apply (aca.hpp:
+ * 202-213) to q (length cols) -> bout (length rows).  Outputs: global pivot ids sigma / tau,
+ * L (unit lower) and U (upper) column-major rank x rank, capacity cap pivots. */
+int hbo_aca_compress(int id, int has_diag, double diag, const double* x, int64_t nt,
+                     const double* y, int64_t ns, int d, int64_t rb, int64_t rows, int64_t cb,
+                     int64_t cols, double eps, int64_t max_rank, int64_t cap, int64_t* sigma,
+                     int64_t* tau, double* L, double* U, int32_t* rank, int32_t* met,
+                     const double* q, double* bout);
 
 #ifdef __cplusplus
 }

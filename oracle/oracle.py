@@ -180,3 +180,105 @@ def rank_problem(d: int, dprime: int | None, kernel: str, n: int, tols, mode: in
     K = assemble(KERNEL_IDS[kernel], x, y, nthreads=nthreads)
     s = singular_values(K)
     return [epsilon_rank_from_sigma(s, t) for t in tols]
+
+
+# ---- ACA (aca.hpp:16-213) and the compiled reference (oracle/_ref) -----------------------------
+REF_LIB = HERE / "_ref" / "libhb_ref.so"
+_ref = None
+_ACA_ARGS = [ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_void_p, ctypes.c_int64,
+             ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_int64, ctypes.c_int64,
+             ctypes.c_int64, ctypes.c_int64, ctypes.c_double, ctypes.c_int64, ctypes.c_int64,
+             ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+             ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32), ctypes.c_void_p,
+             ctypes.c_void_p]
+
+
+def ref_available() -> bool:
+    """True when oracle/_ref/libhb_ref.so (the reference's own headers compiled here) exists."""
+    return REF_LIB.exists()
+
+
+def ref_lib():
+    global _ref
+    if _ref is None:
+        if not REF_LIB.exists():
+            raise OracleError(5, f"{REF_LIB} not built (needs /root/reference; see oracle/Makefile)")
+        L = ctypes.CDLL(str(REF_LIB))
+        L.hbr_aca_compress.argtypes = _ACA_ARGS
+        L.hbr_assemble_dense.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_double,
+                                         ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p,
+                                         ctypes.c_int64, ctypes.c_int, ctypes.c_void_p,
+                                         ctypes.c_int64]
+        L.hbr_eval_radial.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_double,
+                                      ctypes.c_double, ctypes.POINTER(ctypes.c_int)]
+        L.hbr_eval_radial.restype = ctypes.c_double
+        for f in ("hbr_j2", "hbr_y2"):
+            getattr(L, f).argtypes = [ctypes.c_double]
+            getattr(L, f).restype = ctypes.c_double
+        _ref = L
+    return _ref
+
+
+def ref_assemble(kernel_id: int, x: np.ndarray, y: np.ndarray, has_diag: bool = True,
+                 diag: float | None = None, entry_cap: int = 400_000_000) -> np.ndarray:
+    """hodlr::assemble_dense (kernel.hpp:168-181) itself, compiled from /root/reference."""
+    d, T = x.shape
+    _, N = y.shape
+    if diag is None:
+        diag = CATALOG_DIAG.get(kernel_id, 0.0)
+    K = np.empty((T, N), dtype=np.float64, order="F")
+    st = ref_lib().hbr_assemble_dense(kernel_id, int(has_diag), float(diag),
+                                      np.ascontiguousarray(x).ctypes.data, T,
+                                      np.ascontiguousarray(y).ctypes.data, N, d, K.ctypes.data,
+                                      entry_cap)
+    if st:
+        raise OracleError(st, "hbr_assemble_dense")
+    return K
+
+
+@dataclass
+class ACAResult:
+    rank: int
+    met: bool
+    sigma: np.ndarray  # global target ids of the row pivots
+    tau: np.ndarray    # global source ids of the column pivots
+    L: np.ndarray      # rank x rank unit lower
+    U: np.ndarray      # rank x rank upper, pivots on the diagonal
+    b: np.ndarray | None = None  # apply(q) if q was given
+
+
+def aca_compress(kernel_id: int, x: np.ndarray, y: np.ndarray, eps: float, max_rank: int,
+                 rb: int = 0, rows: int | None = None, cb: int = 0, cols: int | None = None,
+                 q: np.ndarray | None = None, has_diag: bool = True, diag: float | None = None,
+                 impl: str = "oracle") -> ACAResult:
+    """hodlr::compress (+ apply) on BlockSpec(kernel, x, rb, rows, y, cb, cols).
+    impl="oracle": the C restatement (hb_oracle.c); impl="ref": the reference's aca.hpp
+    compiled in place (oracle/_ref)."""
+    d, nt = x.shape
+    _, ns = y.shape
+    rows = nt - rb if rows is None else rows
+    cols = ns - cb if cols is None else cols
+    if diag is None:
+        diag = CATALOG_DIAG.get(kernel_id, 0.0)
+    cap = max(1, min(rows, cols, max_rank))
+    sigma = np.zeros(cap, np.int64)
+    tau = np.zeros(cap, np.int64)
+    L = np.zeros(cap * cap)
+    U = np.zeros(cap * cap)
+    rk, met = ctypes.c_int32(0), ctypes.c_int32(0)
+    qq = None if q is None else np.ascontiguousarray(q, dtype=np.float64)
+    b = None if q is None else np.zeros(rows)
+    f = ref_lib().hbr_aca_compress if impl == "ref" else lib().hbo_aca_compress
+    if impl != "ref":
+        f.argtypes = _ACA_ARGS
+    xs, ys = np.ascontiguousarray(x), np.ascontiguousarray(y)
+    st = f(kernel_id, int(has_diag), float(diag), xs.ctypes.data, nt, ys.ctypes.data, ns, d,
+           rb, rows, cb, cols, float(eps), max_rank, cap, sigma.ctypes.data, tau.ctypes.data,
+           L.ctypes.data, U.ctypes.data, ctypes.byref(rk), ctypes.byref(met),
+           None if qq is None else qq.ctypes.data, None if b is None else b.ctypes.data)
+    if st:
+        raise OracleError(st, f"aca_compress[{impl}]")
+    r = rk.value
+    return ACAResult(r, bool(met.value), sigma[:r].copy(), tau[:r].copy(),
+                     L[:r * r].reshape(r, r, order="F").copy(),
+                     U[:r * r].reshape(r, r, order="F").copy(), b)

@@ -1,0 +1,111 @@
+// ref_wrap.cpp -- TEST INFRASTRUCTURE ONLY.  extern "C" wrapper that compiles the reference's
+// own headers (kernel.hpp, aca.hpp, bessel.hpp, types.hpp) from where they lie under
+// /root/reference/proj/include, against the from-scratch Eigen subset in oracle/eigen_shim,
+// into oracle/_ref/libhb_ref.so.  No reference source is copied into this repository.
+// It is the second oracle: tests pin the C restatement (hb_oracle.c) against it, and
+// tests/golden/make_aca_golden.py freezes its outputs as fixtures for the GPU box (where
+// /root/reference does not exist).
+#include <cstdint>
+#include <cstring>
+#include <stdexcept>
+
+#include "hodlr/aca.hpp"
+#include "hodlr/kernel.hpp"
+
+using namespace hodlr;
+
+namespace {
+// status codes of include/hb.h
+enum { OK = 0, EINVAL_ = 1, EDOMAIN_ = 2, ECAP_ = 3, ESINGULAR_ = 4, EUNSUPPORTED_ = 5 };
+
+KernelSpec spec_of(int id, int has_diag, double diag) {
+  KernelSpec s = KernelSpec::catalog(static_cast<KernelId>(id));  // kernel.hpp:42-67
+  if (has_diag)
+    s.diagonal_value = diag;
+  else
+    s.diagonal_value.reset();
+  return s;
+}
+
+PointSet soa_to_pointset(const double* soa, int64_t n, int d) {
+  PointSet p(n, d);  // column-major N x d == SoA
+  std::memcpy(p.data(), soa, sizeof(double) * (size_t)(n * d));
+  return p;
+}
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return OK;
+  } catch (const std::invalid_argument&) {
+    return EINVAL_;
+  } catch (const std::length_error&) {
+    return ECAP_;
+  } catch (const std::domain_error&) {
+    return EDOMAIN_;
+  } catch (const std::runtime_error&) {
+    return ESINGULAR_;
+  } catch (...) {
+    return EUNSUPPORTED_;
+  }
+}
+}  // namespace
+
+extern "C" {
+
+double hbr_eval_radial(int id, int has_diag, double diag, double r, int* status) {
+  double out = 0.0;
+  *status = guarded([&] { out = eval_radial(spec_of(id, has_diag, diag), r); });
+  return out;
+}
+
+double hbr_j2(double x) { return bessel::j2(x); }
+double hbr_y2(double x) { return bessel::y2(x); }
+
+// hodlr::assemble_dense (kernel.hpp:168-181) -> K column-major T x N.
+int hbr_assemble_dense(int id, int has_diag, double diag, const double* x_soa, int64_t T,
+                       const double* y_soa, int64_t N, int d, double* K, int64_t entry_cap) {
+  return guarded([&] {
+    const KernelSpec s = spec_of(id, has_diag, diag);
+    const Matrix k = assemble_dense(s, soa_to_pointset(x_soa, T, d), soa_to_pointset(y_soa, N, d),
+                                    entry_cap);
+    std::memcpy(K, k.data(), sizeof(double) * (size_t)(T * N));
+  });
+}
+
+// hodlr::compress (aca.hpp:171-198) on BlockSpec(kernel, targets, rb, rows, sources, cb, cols)
+// (aca.hpp:26-28), and optionally hodlr::apply (aca.hpp:202-213) to q (length cols) -> b (rows).
+// Outputs: sigma/tau (global ids), L/U column-major r x r, capacity `cap` pivots.
+int hbr_aca_compress(int id, int has_diag, double diag, const double* x_soa, int64_t nt,
+                     const double* y_soa, int64_t ns, int d, int64_t rb, int64_t rows, int64_t cb,
+                     int64_t cols, double eps, int64_t max_rank, int64_t cap, int64_t* sigma,
+                     int64_t* tau, double* L, double* U, int32_t* rank, int32_t* met,
+                     const double* q, double* b) {
+  return guarded([&] {
+    const KernelSpec s = spec_of(id, has_diag, diag);
+    const PointSet X = soa_to_pointset(x_soa, nt, d), Y = soa_to_pointset(y_soa, ns, d);
+    const BlockSpec blk(s, X, rb, rows, Y, cb, cols);
+    const ACAFactor f = compress(blk, eps, max_rank);
+    if (f.rank > cap) throw std::length_error("hbr_aca_compress: capacity");
+    *rank = f.rank;
+    *met = f.tolerance_met ? 1 : 0;
+    for (int k = 0; k < f.rank; ++k) {
+      sigma[k] = f.sigma[(size_t)k];
+      tau[k] = f.tau[(size_t)k];
+    }
+    for (int j = 0; j < f.rank; ++j)
+      for (int i = 0; i < f.rank; ++i) {
+        L[i + (int64_t)j * f.rank] = f.L(i, j);
+        U[i + (int64_t)j * f.rank] = f.U(i, j);
+      }
+    if (q && b) {
+      Vector qq(cols);
+      for (int64_t j = 0; j < cols; ++j) qq(j) = q[j];
+      const Vector bb = apply(f, blk, qq);
+      for (int64_t i = 0; i < rows; ++i) b[i] = bb(i);
+    }
+  });
+}
+
+}  // extern "C"

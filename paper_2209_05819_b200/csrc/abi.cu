@@ -11,6 +11,7 @@
 #include <vector>
 
 #include "context.h"
+#include "bessel_dd.cuh"
 
 namespace {
 
@@ -50,8 +51,6 @@ void check_kernel(const hb_kernel* k) {
   if (k->id < 0 || k->id > HB_K_CUSTOM) throw Error(HB_EINVAL, "unknown kernel id");
   if (k->id == HB_K_CUSTOM)  // kernel.hpp:69-76: std::function cannot cross to the device
     throw Error(HB_EUNSUPPORTED, "Custom kernels (std::function) are not supported on the device");
-  if (k->id == HB_K_HANKEL_H12_RE || k->id == HB_K_HANKEL_H12_IM)
-    throw Error(HB_EUNSUPPORTED, "J2/Y2 (bessel.hpp) are not on the device path");
 }
 
 // integer d-th root of n, or -1
@@ -359,6 +358,8 @@ hb_status hb_eval_radial_host(const hb_kernel* k, double r, double* out) {
       case HB_K_LOG_R: *out = std::log(r); break;
       case HB_K_HELMHOLTZ3D_RE: *out = std::cos(r) / r; break;
       case HB_K_HELMHOLTZ3D_IM: *out = std::sin(r) / r; break;
+      case HB_K_HANKEL_H12_RE: *out = hb::bessel_j2(r); break;  // bessel.hpp:129-135
+      case HB_K_HANKEL_H12_IM: *out = hb::bessel_y2(r); break;  // bessel.hpp:137-144
       case HB_K_R: *out = r; break;
       case HB_K_SIN_R: *out = std::sin(r); break;
       case HB_K_INV_SQRT_1_PLUS_R: *out = 1.0 / std::sqrt(1.0 + r); break;
@@ -599,6 +600,77 @@ hb_status hb_sweep(const hb_problem* probs, int64_t n, const int32_t* devices, i
 }  // extern "C"
 
 #include "hb_debug.h"
+
+namespace {
+void check_aca_args(const hb_kernel* kernel, const double* x, int64_t nt, const double* y, int64_t ns,
+                    int32_t d, const hb_block* b) {
+  check_kernel(kernel);
+  if (!x || !y || !b) throw Error(HB_EINVAL, "aca: NULL argument");
+  if (d < 1 || d > 8) throw Error(HB_EINVAL, "aca: bad dimension");
+  if (b->rows == 0 || b->cols == 0) throw Error(HB_EINVAL, "aca::compress: empty block");  // aca.hpp:174-175
+  if (b->rows < 0 || b->cols < 0 || b->row_begin < 0 || b->col_begin < 0 || b->row_begin + b->rows > nt ||
+      b->col_begin + b->cols > ns)
+    throw Error(HB_EINVAL, "aca: block outside the point sets");
+}
+}  // namespace
+
+extern "C" hb_status hb_aca_compress(hb_context* ctx, const hb_kernel* kernel, const double* d_tgt, int64_t nt,
+                                     const double* d_src, int64_t ns, int32_t d, const hb_block* blocks,
+                                     int64_t nblocks, double eps, int64_t max_rank, hb_aca_factor** out) {
+  if (!ctx || !out) return HB_EINVAL;
+  return guarded(ctx, [&] {
+    if (!(eps > 0)) throw Error(HB_EINVAL, "aca::compress: epsilon must be positive");   // aca.hpp:172
+    if (max_rank < 1) throw Error(HB_EINVAL, "aca::compress: max_rank must be >= 1");  // aca.hpp:173
+    if (nblocks < 1 || !blocks) throw Error(HB_EINVAL, "aca: no blocks");
+    for (int64_t i = 0; i < nblocks; ++i) check_aca_args(kernel, d_tgt, nt, d_src, ns, d, blocks + i);
+    for (int64_t i = 0; i < nblocks; ++i) out[i] = nullptr;
+    HB_CUDA(cudaSetDevice(ctx->device));
+    hb::aca_compress(ctx, *kernel, d_tgt, nt, d_src, ns, d, blocks, nblocks, eps, max_rank, out);
+  });
+}
+
+extern "C" hb_status hb_aca_factor_info(const hb_aca_factor* f, int32_t* rank, int32_t* met, int64_t* mem) {
+  if (!f) return HB_EINVAL;
+  if (rank) *rank = f->rank;
+  if (met) *met = f->met;
+  if (mem)  // aca.hpp:58-61
+    *mem = 2 * (int64_t)f->rank * f->rank * (int64_t)sizeof(double) + 2 * (int64_t)f->rank * (int64_t)sizeof(int64_t);
+  return HB_OK;
+}
+
+extern "C" hb_status hb_aca_factor_copy(const hb_aca_factor* f, int64_t* sigma, int64_t* tau, double* L, double* U) {
+  if (!f) return HB_EINVAL;
+  return guarded(nullptr, [&] {
+    const size_t r = (size_t)f->rank;
+    if (sigma && r) std::memcpy(sigma, f->sigma.data(), r * sizeof(int64_t));
+    if (tau && r) std::memcpy(tau, f->tau.data(), r * sizeof(int64_t));
+    HB_CUDA(cudaSetDevice(f->device));
+    if (L && r) HB_CUDA(cudaMemcpy(L, f->L, r * r * sizeof(double), cudaMemcpyDeviceToHost));
+    if (U && r) HB_CUDA(cudaMemcpy(U, f->U, r * r * sizeof(double), cudaMemcpyDeviceToHost));
+  });
+}
+
+extern "C" hb_status hb_aca_apply(hb_context* ctx, const hb_aca_factor* f, const hb_kernel* kernel,
+                                  const double* d_tgt, int64_t nt, const double* d_src, int64_t ns, int32_t d,
+                                  const hb_block* block, const double* d_q, double* d_b) {
+  if (!ctx || !f) return HB_EINVAL;
+  return guarded(ctx, [&] {
+    check_aca_args(kernel, d_tgt, nt, d_src, ns, d, block);
+    if (!d_q || !d_b) throw Error(HB_EINVAL, "aca::apply: NULL vector");
+    for (int32_t k = 0; k < f->rank; ++k)
+      if (f->sigma[(size_t)k] < block->row_begin || f->sigma[(size_t)k] >= block->row_begin + block->rows ||
+          f->tau[(size_t)k] < block->col_begin || f->tau[(size_t)k] >= block->col_begin + block->cols)
+        throw Error(HB_EINVAL, "aca::apply: factor pivots outside the block");
+    HB_CUDA(cudaSetDevice(ctx->device));
+    hb::aca_apply(ctx, f, *kernel, d_tgt, nt, d_src, ns, d, *block, d_q, d_b);
+  });
+}
+
+extern "C" void hb_aca_factor_destroy(hb_aca_factor* f) {
+  if (!f) return;
+  cudaSetDevice(f->device);
+  delete f;
+}
 
 extern "C" hb_status hb_debug_dgemm_async(hb_context* ctx, int32_t transA, int64_t M, int64_t N,
                                           int64_t K, double alpha, const double* A, int64_t lda,

@@ -12,6 +12,7 @@
 // writes them with 16-byte vector stores, so a warp stores 512 contiguous bytes per column.
 #include "common.cuh"
 #include "kernels.h"
+#include "entries.cuh"
 
 namespace hb {
 
@@ -34,20 +35,6 @@ __global__ void points_kernel(hb_cube cube, int64_t n, int d, int mode, int64_t 
                                           : __ddiv_rn((double)g, (double)(m_axis - 1));
   }
   out[idx] = __dadd_rn(cube.lower[k], __dmul_rn(cube.side, t));
-}
-
-template <int KID>
-__device__ __forceinline__ double radial(double r) {
-  if (KID == HB_K_INVERSE_R) return __ddiv_rn(1.0, r);
-  if (KID == HB_K_LOG_R) return log(r);
-  if (KID == HB_K_HELMHOLTZ3D_RE) return __ddiv_rn(cos(r), r);
-  if (KID == HB_K_HELMHOLTZ3D_IM) return __ddiv_rn(sin(r), r);
-  if (KID == HB_K_R) return r;
-  if (KID == HB_K_SIN_R) return sin(r);
-  if (KID == HB_K_INV_SQRT_1_PLUS_R) return __ddiv_rn(1.0, __dsqrt_rn(__dadd_rn(1.0, r)));
-  if (KID == HB_K_EXP_NEG_R) return exp(-r);
-  if (KID == HB_K_EXP_NEG_R2) return exp(-__dmul_rn(r, r));
-  return 0.0;
 }
 
 constexpr int kTileRows = 128, kTileCols = 64;
@@ -176,6 +163,8 @@ void launch_assemble(const hb_kernel& kern, const double* x, int64_t T, const do
     HB_CASE(HB_K_LOG_R)
     HB_CASE(HB_K_HELMHOLTZ3D_RE)
     HB_CASE(HB_K_HELMHOLTZ3D_IM)
+    HB_CASE(HB_K_HANKEL_H12_RE)
+    HB_CASE(HB_K_HANKEL_H12_IM)
     HB_CASE(HB_K_R)
     HB_CASE(HB_K_SIN_R)
     HB_CASE(HB_K_INV_SQRT_1_PLUS_R)

@@ -41,6 +41,20 @@ struct hb_context {
   double last_sigma1 = 0.0;
 };
 
+// ACAFactor (aca.hpp:50-62) behind the opaque hb_aca_factor handle; L / U stay on the device.
+struct hb_aca_factor {
+  int device = 0;
+  int32_t rank = 0;
+  int32_t met = 1;
+  std::vector<int64_t> sigma, tau;  // global target / source ids
+  double* L = nullptr;              // device, rank x rank column-major (unit lower)
+  double* U = nullptr;              // device, rank x rank column-major (upper)
+  ~hb_aca_factor() {
+    if (L) cudaFree(L);
+    if (U) cudaFree(U);
+  }
+};
+
 namespace hb {
 
 enum BufId {

@@ -46,4 +46,11 @@ void launch_gaussian(double* omega, int64_t rows, int64_t cols, int64_t ld, uint
 
 struct Workspace;  // defined in rank.cu
 
+// ---- ACA (aca.cu) ---------------------------------------------------------------------------
+void aca_compress(hb_context* c, const hb_kernel& kern, const double* x, int64_t nt, const double* y,
+                  int64_t ns, int d, const hb_block* blks, int64_t nb, double eps, int64_t max_rank,
+                  hb_aca_factor** out);
+void aca_apply(hb_context* c, const hb_aca_factor* f, const hb_kernel& kern, const double* x, int64_t nt,
+               const double* y, int64_t ns, int d, const hb_block& blk, const double* q, double* b);
+
 }  // namespace hb

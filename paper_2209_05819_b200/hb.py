@@ -91,6 +91,12 @@ class hb_sweep_opts(ctypes.Structure):
                 ("device_seconds", ctypes.c_double * MAX_DEVICES)]
 
 
+class hb_block(ctypes.Structure):
+    """BlockSpec index ranges (aca.hpp:16-28)."""
+    _fields_ = [("row_begin", ctypes.c_int64), ("rows", ctypes.c_int64),
+                ("col_begin", ctypes.c_int64), ("cols", ctypes.c_int64)]
+
+
 class hb_problem(ctypes.Structure):
     _fields_ = [("kernel", hb_kernel), ("pair", hb_pair), ("tols", ctypes.c_double * MAX_TOLS),
                 ("ntol", ctypes.c_int32), ("reserved", ctypes.c_int32)]
@@ -105,6 +111,9 @@ EXPORTS = [
     "hb_stats_get", "hb_stats_reset", "hb_sweep_ex", "hb_sweep_release", "hb_context_set_stopping",
     # include/hb_debug.h (test hooks)
     "hb_debug_dgemm", "hb_debug_dgemm_async",
+    # ACA (aca.hpp)
+    "hb_aca_compress", "hb_aca_factor_info", "hb_aca_factor_copy", "hb_aca_apply",
+    "hb_aca_factor_destroy",
 ]
 
 _lib = None
@@ -169,6 +178,19 @@ def load(path: os.PathLike | str | None = None):
           c_p, ctypes.c_int64, c_p, ctypes.c_int64, ctypes.c_double, c_p, ctypes.c_int64]
     L.hb_debug_dgemm.argtypes = dg
     L.hb_debug_dgemm_async.argtypes = dg + [ctypes.c_int32]
+    L.hb_aca_compress.argtypes = [c_p, ctypes.POINTER(hb_kernel), c_p, ctypes.c_int64, c_p,
+                                  ctypes.c_int64, ctypes.c_int32, ctypes.POINTER(hb_block),
+                                  ctypes.c_int64, ctypes.c_double, ctypes.c_int64,
+                                  ctypes.POINTER(c_p)]
+    L.hb_aca_factor_info.argtypes = [c_p, ctypes.POINTER(ctypes.c_int32),
+                                     ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int64)]
+    L.hb_aca_factor_copy.argtypes = [c_p, c_p, c_p, c_p, c_p]
+    L.hb_aca_apply.argtypes = [c_p, c_p, ctypes.POINTER(hb_kernel), c_p, ctypes.c_int64, c_p,
+                               ctypes.c_int64, ctypes.c_int32, ctypes.POINTER(hb_block), c_p, c_p]
+    L.hb_aca_factor_destroy.argtypes = [c_p]
+    L.hb_aca_factor_destroy.restype = None
+    for name in ("hb_aca_compress", "hb_aca_factor_info", "hb_aca_factor_copy", "hb_aca_apply"):
+        getattr(L, name).restype = ctypes.c_int
     for name in ("hb_context_create", "hb_context_set_tuning", "hb_generate_points",
                  "hb_assemble", "hb_eval_radial_host", "hb_rank_matrix", "hb_rank",
                  "hb_last_sigma", "hb_sweep", "hb_partition", "hb_context_set_profiling",
@@ -358,6 +380,24 @@ class Context:
             _check(self._lib.hb_debug_dgemm(self._h, int(transA), M, N, K, alpha, A, lda, B, ldb,
                                             beta, C, ldc), "dgemm", self._h)
 
+    def aca_compress(self, kernel: hb_kernel, d_tgt: int, nt: int, d_src: int, ns: int, d: int,
+                     blocks, eps: float, max_rank: int) -> list["ACAFactor"]:
+        """hodlr::compress (aca.hpp:171-198) of each block (hb_block or (rb, rows, cb, cols))."""
+        bl = [b if isinstance(b, hb_block) else hb_block(*b) for b in blocks]
+        arr = (hb_block * max(len(bl), 1))(*bl)
+        out = (ctypes.c_void_p * max(len(bl), 1))()
+        _check(self._lib.hb_aca_compress(self._h, ctypes.byref(kernel), d_tgt, nt, d_src, ns, d,
+                                         arr, len(bl), eps, max_rank, out), "hb_aca_compress",
+               self._h)
+        return [ACAFactor(self._lib, out[i], bl[i]) for i in range(len(bl))]
+
+    def aca_apply(self, f: "ACAFactor", kernel: hb_kernel, d_tgt: int, nt: int, d_src: int,
+                  ns: int, d: int, d_q: int, d_b: int, block: hb_block | None = None):
+        """hodlr::apply (aca.hpp:202-213): b = K(I,τ) U⁻¹ L⁻¹ K(σ,J) q on device vectors."""
+        blk = f.block if block is None else block
+        _check(self._lib.hb_aca_apply(self._h, f._h, ctypes.byref(kernel), d_tgt, nt, d_src, ns, d,
+                                      ctypes.byref(blk), d_q, d_b), "hb_aca_apply", self._h)
+
     def last_sigma(self, max_count: int | None = None) -> list[float]:
         cnt = ctypes.c_int64()
         _check(self._lib.hb_last_sigma(self._h, None, 0, ctypes.byref(cnt)), "hb_last_sigma",
@@ -367,6 +407,43 @@ class Context:
         _check(self._lib.hb_last_sigma(self._h, buf, k, ctypes.byref(cnt)), "hb_last_sigma",
                self._h)
         return list(buf[:k])
+
+
+class ACAFactor:
+    """hodlr::ACAFactor (aca.hpp:50-62): pivots, unit-lower L and upper U stay on the device;
+    .sigma / .tau / .L / .U copy them out (numpy)."""
+
+    def __init__(self, lib, handle, block: hb_block):
+        self._lib = lib
+        self._h = ctypes.c_void_p(handle)
+        self.block = block
+        r, met, mem = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int64()
+        _check(lib.hb_aca_factor_info(self._h, ctypes.byref(r), ctypes.byref(met), ctypes.byref(mem)),
+               "hb_aca_factor_info")
+        self.rank, self.tolerance_met, self.memory_bytes = r.value, bool(met.value), mem.value
+
+    def arrays(self):
+        import numpy as np
+        r = self.rank
+        sig = np.zeros(max(r, 1), np.int64)
+        tau = np.zeros(max(r, 1), np.int64)
+        L = np.zeros(max(r * r, 1))
+        U = np.zeros(max(r * r, 1))
+        _check(self._lib.hb_aca_factor_copy(self._h, sig.ctypes.data, tau.ctypes.data,
+                                            L.ctypes.data, U.ctypes.data), "hb_aca_factor_copy")
+        return (sig[:r], tau[:r], L[:r * r].reshape(r, r, order="F"),
+                U[:r * r].reshape(r, r, order="F"))
+
+    def close(self):
+        if self._h:
+            self._lib.hb_aca_factor_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def partition(problems: Sequence[hb_problem], nparts: int) -> list[int]:

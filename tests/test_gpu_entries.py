@@ -54,8 +54,8 @@ def test_distance_bit_exact(ctx, hb, oracle, d, dp, n, m):
     assert np.array_equal(Kg, Ko)
 
 
-KERNELS = ["one_over_r", "log_r", "helmholtz3d_re", "helmholtz3d_im", "r", "sin_r",
-           "inv_sqrt_1_plus_r", "exp_neg_r", "exp_neg_r2"]
+KERNELS = ["one_over_r", "log_r", "helmholtz3d_re", "helmholtz3d_im", "hankel_h12_re",
+           "hankel_h12_im", "r", "sin_r", "inv_sqrt_1_plus_r", "exp_neg_r", "exp_neg_r2"]
 
 
 @pytest.mark.parametrize("kname", KERNELS)
@@ -70,6 +70,27 @@ def test_entries_within_tolerance(ctx, hb, oracle, kname, d, dp, n, mode):
     rel = np.abs(Kg - Ko) / np.where(both_zero, 1.0, np.abs(Ko))
     assert np.all(np.isfinite(Kg))
     assert rel.max() <= TOL_REL, f"max rel {rel.max():.3e}"
+
+
+@pytest.mark.parametrize("kname", ["hankel_h12_re", "hankel_h12_im"])
+def test_bessel_entries(ctx, hb, oracle, kname):
+    """J2 / Y2 (bessel.hpp:129-144) in double-double on the device vs the oracle's __float128 /
+    long double restatement (itself bit-identical to the reference's bessel.hpp, test_oracle.py):
+    series branch (r <= 19) within 2 ulp + 1e-300, asymptotic branch (r > 19) within
+    8e-16 * sqrt(2 / (pi r)) absolute — the reference evaluates cos / sin of x - (2nu+1)pi/4 in
+    long double, the device from sincos(x) and the exact +-sqrt(2)/2."""
+    n = 1500
+    x = np.zeros((1, n))
+    y = np.concatenate([np.geomspace(1e-6, 19.0, 1000), np.linspace(19.0 + 1e-9, 120.0, 500)])[None, :]
+    X, Y = torch.from_numpy(x).cuda(), torch.from_numpy(np.ascontiguousarray(y)).cuda()
+    torch.cuda.synchronize()
+    Kg = dev_assemble(ctx, hb, hb.make_kernel(kname), X[:, :1].contiguous(), Y)[0]
+    Ko = oracle.assemble(oracle.KERNEL_IDS[kname], x[:, :1], y)[0]
+    r = y[0]
+    ser = r <= 19.0
+    ulp = np.spacing(np.abs(Ko))
+    assert np.all(np.abs(Kg - Ko)[ser] <= 2 * ulp[ser] + 1e-300)
+    assert np.all(np.abs(Kg - Ko)[~ser] <= 8e-16 * np.sqrt(2 / (np.pi * r[~ser])))
 
 
 def test_diagonal_rule(ctx, hb, oracle):
@@ -91,10 +112,12 @@ def test_assemble_errors(ctx, hb):
     with pytest.raises(hb.HBError) as e:
         dev_assemble(ctx, hb, hb.make_kernel("one_over_r", diagonal=None), X, X)
     assert e.value.status == 4  # ESINGULAR (kernel.hpp:152-153)
-    for kname in ("custom", "hankel_h12_re"):
-        with pytest.raises(hb.HBError) as e:
-            dev_assemble(ctx, hb, hb.make_kernel(kname), X, X)
-        assert e.value.status == 5
+    with pytest.raises(hb.HBError) as e:
+        dev_assemble(ctx, hb, hb.make_kernel("custom"), X, X)
+    assert e.value.status == 5
+    with pytest.raises(hb.HBError) as e:  # Y2 is singular at 0 (kernel.hpp:80), no diagonal given
+        dev_assemble(ctx, hb, hb.make_kernel("hankel_h12_im", diagonal=None), X, X)
+    assert e.value.status == 4
     K = torch.empty(16 * 16, dtype=torch.float64, device="cuda")
     with pytest.raises(hb.HBError) as e:
         ctx.assemble(hb.make_kernel("log_r"), X.data_ptr(), 16, X.data_ptr(), 16, 2, K.data_ptr(), 8)

@@ -68,9 +68,25 @@ def test_entry_cap_and_errors(oracle):
     assert e.value.status == 3  # length_error -> ECAP (kernel.hpp:174-175)
     with pytest.raises(O.OracleError):
         O.assemble(O.KERNEL_IDS["log_r"], np.zeros((2, 3)), np.zeros((3, 3)))
-    with pytest.raises(O.OracleError) as e:
-        O.assemble(O.KERNEL_IDS["hankel_h12_re"], x, y + 1)
+    with pytest.raises(O.OracleError) as e:  # Custom (std::function) has no restatement
+        O.assemble(11, x, y + 1)
     assert e.value.status == 5
+
+
+def test_bessel_j2_y2_bit_exact_vs_reference(oracle):
+    """J2 / Y2 restated (__float128 series, long double asymptotics) equal the reference's own
+    bessel.hpp compiled in place, bit for bit, on both branches."""
+    import ctypes
+    if not oracle.ref_available():
+        pytest.skip("oracle/_ref not built (needs /root/reference)")
+    L, R = oracle.lib(), oracle.ref_lib()
+    for f in (L.hbo_j2, L.hbo_y2):
+        f.argtypes = [ctypes.c_double]
+        f.restype = ctypes.c_double
+    xs = np.concatenate([np.geomspace(1e-9, 19.0, 3000), np.linspace(19.0, 150.0, 3000), [19.0, 19.000000001]])
+    assert all(L.hbo_j2(float(v)) == R.hbr_j2(float(v)) for v in xs)
+    assert all(L.hbo_y2(float(v)) == R.hbr_y2(float(v)) for v in xs)
+    assert L.hbo_j2(0.0) == 0.0
 
 
 # ---- point generator ---------------------------------------------------------------------
