@@ -10,8 +10,12 @@ assemble K, sketch-pivoted QR, certify the ε-rank.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload sweep|d1|d2|d3|d4]
 
-N > 1 runs under torchrun (one process per GPU, NCCL only for the final result gather); the
-problems are LPT-partitioned (hb_partition), total work is fixed -> strong scaling.
+N > 1 runs under torchrun (one process per GPU, NCCL only for the final result gather).
+Per-config workloads (c0..c3, default c1) scale WEAK: every rank runs the whole config on its
+own independent problems (per-problem seeds from base seed = rank; rank 0's are the golden ones),
+so the work per GPU is fixed and `value` = all ranks' entries / max-over-ranks device time.
+The full sweep (configs[4], which BASELINE.json states as partitioned across 1/2/4/8 B200) is
+LPT-partitioned over the ranks (hb_partition): total work fixed -> strong scaling.
 """
 from __future__ import annotations
 
@@ -71,8 +75,8 @@ def workload(name: str):
     return probs
 
 
-def to_problems(hb, wl):
-    return [hb.make_problem(k, d, dp, n, tols, base_seed=0) for (d, dp, k, n, tols) in wl]
+def to_problems(hb, wl, base_seed: int = 0):
+    return [hb.make_problem(k, d, dp, n, tols, base_seed=base_seed) for (d, dp, k, n, tols) in wl]
 
 
 def alg_flops(n: int, p: int, kernel: str) -> float:
@@ -218,7 +222,10 @@ def main():
            "entries_per_step": sum(n * n for (_, _, _, n, _) in wl),
            "l2": "inputs larger than L2: every step regenerates points and re-assembles K (sum 8N^2 = "
                  f"{8 * sum(n * n for (_, _, _, n, _) in wl) / 1e12:.2f} TB written per step)",
-           "parallelism": f"lpt-partition x{world}"}
+           "parallelism": (f"replicated config x{world} (independent seeds per rank)"
+                           if args.workload != "sweep" else f"lpt-partition x{world}")}
+    if args.workload != "sweep":
+        cfg["entries_per_step_whole_job"] = cfg["entries_per_step"] * world
     sample = [w for w in wl if w[3] <= args.cpu_sample_max_n]
 
     if args.impl == "reference":
@@ -237,7 +244,8 @@ def main():
         line = {"impl": "reference", "metric": METRIC, "value": round(v, 6), "unit": "G entries/s",
                 "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
                 "ms_per_step": round(1e3 * statistics.median(dts), 1), "higher_is_better": True,
-                "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "scaling": "strong" if args.workload == "sweep" else "weak", "vs_baseline": None,
+                "dtype": "f64", "data": "synthetic",
                 "config": cfg,
                 "cpu_baseline": {"value": round(v, 6), "unit": "G entries/s", "cores": threads,
                                  "kind": "port",
@@ -259,8 +267,13 @@ def main():
         dist = None
         torch.cuda.set_device(local)
     dev = local
-    problems = to_problems(hb, wl)
-    mine = hbd.my_share(problems, rank, world)
+    weak = args.workload != "sweep"
+    if weak:  # every rank: the whole config on its own seeds (rank 0 = the golden seeds)
+        problems = [pr for r in range(world) for pr in to_problems(hb, wl, base_seed=r)]
+        mine = list(range(rank * len(wl), (rank + 1) * len(wl)))
+    else:
+        problems = to_problems(hb, wl)
+        mine = hbd.my_share(problems, rank, world)
     my_probs = [problems[i] for i in mine]
 
     def barrier():
@@ -303,7 +316,7 @@ def main():
         dist.destroy_process_group()
         return 0
 
-    entries = cfg["entries_per_step"]
+    entries = cfg["entries_per_step"] * (world if weak else 1)
     value = entries * args.steps / t_dev / 1e9
     e2e = entries * args.steps / t_wall / 1e9
     peak, peak_src = fp64_peak()
@@ -313,10 +326,11 @@ def main():
     checked = equal = 0
     mism = []
     total_alg = 0.0
-    for (d, dp, k, n, tols), res in zip(wl, full):
+    for j, res in enumerate(full):
+        d, dp, k, n, tols = wl[j % len(wl)]
         for t, r in enumerate(res):
             total_alg += alg_flops(n, r.rank, k) if t == 0 else 0.0
-        g = gm.get((d, dp, k, n))
+        g = gm.get((d, dp, k, n)) if j < len(wl) else None  # golden seeds: rank 0's copy
         if g:
             for t, r in enumerate(res):
                 checked += 1
@@ -332,11 +346,12 @@ def main():
     line = {
         "metric": METRIC, "value": round(value, 4), "unit": "G entries/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * t_dev / args.steps, 1),
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": cfg,
+        "higher_is_better": True, "scaling": "weak" if weak else "strong", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic", "config": cfg,
         "e2e": {"value": round(e2e, 4), "unit": "G entries/s",
                 "h2d_bytes_per_step": len(problems) * __import__("ctypes").sizeof(hb.hb_problem),
                 "d2h_bytes_per_step": sum(p.ntol for p in problems) * __import__("ctypes").sizeof(hb.hb_rank_result),
+                "note": "whole job (all ranks)",
                 "api": "hb_sweep_ex (C ABI) from host descriptors to host result records; points are "
                        "generated on device from the seeds (k1)"},
         "roofline": {"bound": "tensor", "kernel": "dgemm_kernel (FP64 DMMA m8n8k4; trailing update, "
@@ -353,7 +368,7 @@ def main():
         "parity": {"checked_vs_oracle": checked, "equal": equal, "mismatches": mism[:20],
                    "uncertified_brackets": uncert, "probabilistic_certificates": prob_cert,
                    "statuses_ok": all(s == 0 for s in statuses),
-                   "failed": [[list(w[:4]), s] for w, s in zip([wl[i] for i in mine], statuses) if s != 0][:10],
+                   "failed": [[list(w[:4]), s] for w, s in zip([wl[i % len(wl)] for i in mine], statuses) if s != 0][:10],
                    "last_error": hb.load().hb_last_error(None).decode()[:200]},
         "phase_ms": {k: round(v, 1) for k, v in stats["phase_ms"].items()},
         "gemm_ms": round(stats["gemm_ms"], 1),

@@ -528,7 +528,8 @@ hb_status hb_sweep_ex(const hb_problem* probs, int64_t n, const int32_t* devices
     if (!small.empty()) {
       std::atomic<size_t> next{0};  // set to nsub below: sub-stream s starts with small[s]
       cudaEvent_t ready;
-      cudaEventCreateWithFlags(&ready, cudaEventDisableTiming);
+      if (getenv("HB_TIMELINE")) cudaEventCreate(&ready);
+      else cudaEventCreateWithFlags(&ready, cudaEventDisableTiming);
       cudaEventRecord(ready, c->stream);
       const int nsub = (int)std::min<size_t>(sub_streams(), small.size());
       next = (size_t)nsub;
@@ -554,14 +555,37 @@ hb_status hb_sweep_ex(const hb_problem* probs, int64_t n, const int32_t* devices
           hb::context_set_priority(sc, (s == 0 && nsub > 1) ? hi : lo);
         } catch (const hb::Error&) {
         }
-        const int half = c->num_sms / 2;
+        static const double crit_share = [] {  // SM share of the critical stream's coop grids
+          const char* e = getenv("HB_CRIT_SHARE");
+          const double v = e ? atof(e) : 0.5;
+          return v < 0.1 ? 0.1 : (v > 0.9 ? 0.9 : v);
+        }();
+        const int half = std::max(1, (int)(c->num_sms * crit_share));
         sc->coop_sms = nsub == 1 ? c->num_sms
                                  : (s == 0 ? half : std::max(1, (c->num_sms - half) / (nsub - 1)));
         sc->profiling = c->profiling;
         cudaStreamWaitEvent(sc->stream, ready, 0);
+        static const bool timeline = getenv("HB_TIMELINE") != nullptr;
         for (size_t q = (size_t)s; q < small.size(); q = next.fetch_add(1)) {
           const hb_problem& p = probs[small[q]];
+          cudaEvent_t e0 = nullptr, e1 = nullptr;
+          if (timeline) {
+            cudaEventCreate(&e0);
+            cudaEventCreate(&e1);
+            cudaEventRecord(e0, sc->stream);
+          }
           st[small[q]] = hb_rank(sc, &p.kernel, &p.pair, p.tols, p.ntol, out + offset[small[q]]);
+          if (timeline) {  // HB_TIMELINE=1: per-problem device span on its sub-stream (stderr)
+            cudaEventRecord(e1, sc->stream);
+            cudaEventSynchronize(e1);
+            float a = 0.f, b = 0.f;
+            cudaEventElapsedTime(&a, ready, e0);
+            cudaEventElapsedTime(&b, ready, e1);
+            fprintf(stderr, "[timeline] stream %d N=%lld d=%d d'=%d start %.2f end %.2f ms\n", s,
+                    (long long)p.pair.n_target, p.pair.target.d, p.pair.d_prime, a, b);
+            cudaEventDestroy(e0);
+            cudaEventDestroy(e1);
+          }
         }
         cudaEventRecord(sc->ev[5], sc->stream);
       };
