@@ -526,20 +526,35 @@ hb_status hb_sweep_ex(const hb_problem* probs, int64_t n, const int32_t* devices
     }
     std::vector<hb_context*> subs;
     if (!small.empty()) {
-      std::atomic<size_t> next{0};  // set to nsub below: sub-stream s starts with small[s]
       cudaEvent_t ready;
       if (getenv("HB_TIMELINE")) cudaEventCreate(&ready);
       else cudaEventCreateWithFlags(&ready, cudaEventDisableTiming);
       cudaEventRecord(ready, c->stream);
       const int nsub = (int)std::min<size_t>(sub_streams(), small.size());
-      next = (size_t)nsub;
+      // two-ended queue: the first nsub - nback streams take the costliest remaining problem, the
+      // last nback streams the cheapest (latency-bound small problems start at t = 0 instead of
+      // forming a tail after the large ones); HB_BACK_STREAMS, default 0
+      static const int back_env = [] {
+        const char* e = getenv("HB_BACK_STREAMS");
+        return e ? std::max(0, atoi(e)) : 0;
+      }();
+      const int nback = std::min(back_env, nsub - 1);
+      std::mutex q_mu;
+      int64_t q_front = 0, q_back = (int64_t)small.size() - 1;
+      auto take = [&](bool from_back) -> int64_t {
+        std::lock_guard<std::mutex> lk(q_mu);
+        if (q_front > q_back) return -1;
+        return from_back ? q_back-- : q_front++;
+      };
+      std::vector<int64_t> first_q(nsub);  // stream 0 starts with the costliest problem
+      for (int s = 0; s < nsub; ++s) first_q[s] = take(s >= nsub - nback);
       std::vector<std::thread> sth;
       std::mutex sub_mu;
       auto sub_worker = [&](int s) {
         hb_status ss = HB_OK;
         hb_context* sc = cached_context(devices[w], 1000 + slot[w] * 16 + s, &ss);
         if (!sc) {
-          for (size_t q = (size_t)s; q < small.size(); q = next.fetch_add(1)) st[small[q]] = ss;
+          for (int64_t q = first_q[s]; q >= 0; q = take(s >= nsub - nback)) st[small[q]] = ss;
           return;
         }
         {
@@ -566,7 +581,8 @@ hb_status hb_sweep_ex(const hb_problem* probs, int64_t n, const int32_t* devices
         sc->profiling = c->profiling;
         cudaStreamWaitEvent(sc->stream, ready, 0);
         static const bool timeline = getenv("HB_TIMELINE") != nullptr;
-        for (size_t q = (size_t)s; q < small.size(); q = next.fetch_add(1)) {
+        const bool from_back = s >= nsub - nback;
+        for (int64_t q = first_q[s]; q >= 0; q = take(from_back)) {
           const hb_problem& p = probs[small[q]];
           cudaEvent_t e0 = nullptr, e1 = nullptr;
           if (timeline) {

@@ -108,6 +108,7 @@ __global__ void band_extract_kernel(const double* M, int64_t ldm, int64_t k, int
 __global__ void band_bidiag_out(const double* Bd, int64_t k, int nb, double* d, double* e);
 __global__ void bulge_chase_kernel(double* Bd, int64_t k, int nb, int* prog);
 __global__ void bidiag_small_kernel(const double* Mk, int64_t ldm, int k, double* d, double* e);
+constexpr int kSmallBidiagThreads = 512;
 constexpr int kSmallBidiag = 144;  // k x k triangle up to this size: one-CTA shared-memory bidiag
 // Mid-size k: one thread-block cluster holds the triangle in distributed shared memory
 // (bidiag_cluster.cu).  bidiag_cluster_size(k) = cluster size to use (8 or 16), 0 = does not fit.

@@ -287,7 +287,7 @@ void two_stage_bidiag(hb_context* c, double* Mk, int64_t ldm, int64_t k, double*
   if (k <= kSmallBidiag) {  // one CTA, whole triangle in shared memory
     const size_t smem = ((size_t)k * (k + 1) + 3 * (size_t)k) * sizeof(double);
     ensure_dyn_smem((const void*)bidiag_small_kernel, smem);
-    bidiag_small_kernel<<<1, 256, smem, st>>>(Mk, ldm, (int)k, d, e);
+    bidiag_small_kernel<<<1, kSmallBidiagThreads, smem, st>>>(Mk, ldm, (int)k, d, e);
     HB_LAUNCH_CHECK();
     return;
   }

@@ -624,9 +624,11 @@ namespace hb {
 // memory and runs the one-stage Golub–Kahan bidiagonalisation there (no grid barriers, one
 // launch).  Column-major with odd leading dimension k+1 so column sweeps (w = uᵀM) and row sweeps
 // (z = M v) are both bank-conflict free.
-__global__ void __launch_bounds__(256) bidiag_small_kernel(const double* __restrict__ Mk, int64_t ldm,
-                                                           int k, double* __restrict__ d,
-                                                           double* __restrict__ e) {
+__global__ void __launch_bounds__(kSmallBidiagThreads) bidiag_small_kernel(const double* __restrict__ Mk,
+                                                                         int64_t ldm, int k,
+                                                                         double* __restrict__ d,
+                                                                         double* __restrict__ e) {
+  constexpr int NT = kSmallBidiagThreads, NW = NT / 32, NG = NT / 4;
   extern __shared__ double S[];  // [k][k+1] + u[k] + v[k] + w[k]
   const int ld = k + 1;
   double* u = S + (size_t)k * ld;
@@ -634,7 +636,8 @@ __global__ void __launch_bounds__(256) bidiag_small_kernel(const double* __restr
   double* w = vv + k;
   __shared__ double sh[4];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int idx = tid; idx < k * k; idx += 256) {
+  const int sub = lane & 3, grp = tid >> 2;  // 4 lanes per dot product
+  for (int idx = tid; idx < k * k; idx += NT) {
     const int r = idx % k, c = idx / k;
     S[c * ld + r] = Mk[r + (int64_t)c * ldm];
   }
@@ -657,15 +660,21 @@ __global__ void __launch_bounds__(256) bidiag_small_kernel(const double* __restr
     }
     __syncthreads();
     const double tu = sh[0];
-    for (int q = i + 1 + tid; q < k; q += 256) {
+    // w[q] = tu · Σ_{r >= i} u[r] S[r, q]  (q > i), four lanes per column, fixed order
+    for (int q0 = i + 1; q0 < k; q0 += NG) {
+      const int q = q0 + grp;
       double s = 0.0;
-      for (int r = i; r < k; ++r) s += u[r] * S[q * ld + r];
-      w[q] = s * tu;
+      if (q < k)
+        for (int r = i + sub; r < k; r += 4) s += u[r] * S[q * ld + r];
+      s += __shfl_xor_sync(0xffffffffu, s, 1);
+      s += __shfl_xor_sync(0xffffffffu, s, 2);
+      if (q < k && sub == 0) w[q] = s * tu;
     }
     __syncthreads();
-    for (int idx = tid; idx < (k - i) * (k - i - 1); idx += 256) {
-      const int r = i + idx % (k - i), q = i + 1 + idx / (k - i);
-      S[q * ld + r] -= u[r] * w[q];
+    for (int q = i + 1 + warp; q < k; q += NW) {
+      const double wq = w[q];
+      double* Sq = S + q * ld;
+      for (int r = i + lane; r < k; r += 32) Sq[r] -= u[r] * wq;
     }
     __syncthreads();
     if (i + 1 >= k) break;
@@ -686,15 +695,21 @@ __global__ void __launch_bounds__(256) bidiag_small_kernel(const double* __restr
     }
     __syncthreads();
     const double tv = sh[1];
-    for (int r = i + 1 + tid; r < k; r += 256) {
+    // w[r] = tv · Σ_{q > i} S[r, q] vv[q]  (r > i), four lanes per row, fixed order
+    for (int r0 = i + 1; r0 < k; r0 += NG) {
+      const int r = r0 + grp;
       double s = 0.0;
-      for (int q = i + 1; q < k; ++q) s += S[q * ld + r] * vv[q];
-      w[r] = s * tv;
+      if (r < k)
+        for (int q = i + 1 + sub; q < k; q += 4) s += S[q * ld + r] * vv[q];
+      s += __shfl_xor_sync(0xffffffffu, s, 1);
+      s += __shfl_xor_sync(0xffffffffu, s, 2);
+      if (r < k && sub == 0) w[r] = s * tv;
     }
     __syncthreads();
-    for (int idx = tid; idx < (k - i - 1) * (k - i - 1); idx += 256) {
-      const int r = i + 1 + idx % (k - i - 1), q = i + 1 + idx / (k - i - 1);
-      S[q * ld + r] -= w[r] * vv[q];
+    for (int q = i + 1 + warp; q < k; q += NW) {
+      const double vq = vv[q];
+      double* Sq = S + q * ld;
+      for (int r = i + 1 + lane; r < k; r += 32) Sq[r] -= w[r] * vq;
     }
     __syncthreads();
   }
