@@ -17,6 +17,7 @@
 
 #include <cstdint>
 #include <optional>
+#include <memory>
 #include <ostream>
 #include <stdexcept>
 #include <string>
@@ -303,6 +304,79 @@ inline void write_csv_row(std::ostream& os, const RankRecord& r) {
      << (r.interaction.is_far() ? -1 : r.interaction.surface_dim) << ',' << r.N << ',' << r.epsilon
      << ',' << r.rank << ',' << r.seconds << ',' << r.rank_lo << ',' << r.rank_hi << ','
      << r.k_factored << ',' << r.sigma1 << ',' << r.gap << '\n';
+}
+
+// ---- ACA (aca.hpp:16-213) on device point sets --------------------------------------------------
+// BlockSpec: K(I, J) over SoA device point sets (coordinate k of point i at k*n + i).
+struct BlockSpec {  // aca.hpp:16-28
+  const KernelSpec* kernel = nullptr;
+  const double* targets = nullptr;  // device, d x nt
+  const double* sources = nullptr;  // device, d x ns
+  int64_t nt = 0, ns = 0;
+  int d = 0;
+  int64_t row_begin = 0, rows = 0, col_begin = 0, cols = 0;
+  hb_block to_c() const { return hb_block{row_begin, rows, col_begin, cols}; }
+};
+
+// ACAFactor (aca.hpp:50-62): pivot ids and r x r LU factors (host copies; the device handle
+// stays alive for apply()).
+struct ACAFactor {
+  std::vector<int64_t> sigma, tau;
+  std::vector<double> L, U;  // column-major rank x rank
+  int rank = 0;
+  bool tolerance_met = true;
+  std::shared_ptr<hb_aca_factor> handle;
+  int64_t memory_bytes() const {  // aca.hpp:58-61
+    return 2 * (int64_t)rank * rank * (int64_t)sizeof(double) + 2 * (int64_t)rank * (int64_t)sizeof(int64_t);
+  }
+};
+
+// compress (aca.hpp:171-198) of several blocks of the same point sets in one call.
+inline std::vector<ACAFactor> compress(Device& dev, const std::vector<BlockSpec>& blocks, double epsilon,
+                                       int64_t max_rank) {
+  if (blocks.empty()) return {};
+  const BlockSpec& b0 = blocks.front();
+  if (!b0.kernel) throw std::invalid_argument("aca::compress: BlockSpec without a kernel");
+  std::vector<hb_block> cb;
+  for (const auto& b : blocks) {
+    if (b.kernel != b0.kernel || b.targets != b0.targets || b.sources != b0.sources)
+      throw std::invalid_argument("aca::compress: blocks of one call share kernel and point sets");
+    cb.push_back(b.to_c());
+  }
+  const hb_kernel ck = b0.kernel->to_c();
+  std::vector<hb_aca_factor*> raw(blocks.size(), nullptr);
+  check(hb_aca_compress(dev.get(), &ck, b0.targets, b0.nt, b0.sources, b0.ns, b0.d, cb.data(),
+                        (int64_t)cb.size(), epsilon, max_rank, raw.data()),
+        "aca::compress", dev.get());
+  std::vector<ACAFactor> out;
+  for (hb_aca_factor* h : raw) {
+    ACAFactor f;
+    f.handle = std::shared_ptr<hb_aca_factor>(h, hb_aca_factor_destroy);
+    int32_t r = 0, met = 0;
+    check(hb_aca_factor_info(h, &r, &met, nullptr), "aca::compress");
+    f.rank = r;
+    f.tolerance_met = met != 0;
+    f.sigma.resize(r);
+    f.tau.resize(r);
+    f.L.resize((size_t)r * r);
+    f.U.resize((size_t)r * r);
+    check(hb_aca_factor_copy(h, f.sigma.data(), f.tau.data(), f.L.data(), f.U.data()), "aca::compress");
+    out.push_back(std::move(f));
+  }
+  return out;
+}
+
+inline ACAFactor compress(Device& dev, const BlockSpec& block, double epsilon, int64_t max_rank) {
+  return compress(dev, std::vector<BlockSpec>{block}, epsilon, max_rank).front();
+}
+
+// apply (aca.hpp:202-213): b = K(I, τ) U⁻¹ L⁻¹ K(σ, J) q for device vectors q (cols), b (rows).
+inline void apply(Device& dev, const ACAFactor& f, const BlockSpec& block, const double* d_q, double* d_b) {
+  const hb_kernel ck = block.kernel->to_c();
+  const hb_block cb = block.to_c();
+  check(hb_aca_apply(dev.get(), f.handle.get(), &ck, block.targets, block.nt, block.sources, block.ns,
+                     block.d, &cb, d_q, d_b),
+        "aca::apply", dev.get());
 }
 
 }  // namespace hb200
