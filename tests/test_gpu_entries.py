@@ -155,3 +155,25 @@ def test_dgemm_hook_numerics(ctx, hb):
                   Ccm.data_ptr(), M)
         err = (Ccm.t() - ref).abs().max().item() / max(ref.abs().max().item(), 1e-300)
         assert err < 1e-14 * max(1.0, K ** 0.5), (ta, M, N, K, err)
+
+
+@pytest.mark.parametrize("M,N,K,ldpad", [(5000, 333, 120, 0), (1000, 1000, 64, 0), (777, 4097, 117, 3),
+                                         (4096, 257, 8, 1), (300, 300, 1, 0), (2048, 2048, 128, 0),
+                                         (16001, 1500, 97, 5), (4000, 4000, 120, 0),
+                                         (3000, 3500, 64, 1), (9000, 1100, 1, 0), (5003, 4001, 30, 2)])
+def test_update_gemm_numerics(ctx, hb, M, N, K, ldpad):
+    """The rank-b trailing-update shape C -= A B (K <= 128) of the DMMA GEMM against torch fp64:
+    odd K, ragged M / N, odd leading dimensions (8-byte path), K not a multiple of the k-tile."""
+    g = torch.Generator(device="cuda").manual_seed(K)
+    lda, ldb, ldc = M + ldpad, K + ldpad, M + ldpad
+    A = torch.randn((K, lda), dtype=torch.float64, device="cuda", generator=g)  # column-major M x K
+    B = torch.randn((N, ldb), dtype=torch.float64, device="cuda", generator=g)  # column-major K x N
+    C = torch.randn((N, ldc), dtype=torch.float64, device="cuda", generator=g)  # column-major M x N
+    ref = C[:, :M].t() - A[:, :M].t() @ B[:, :K].t()
+    keep = C[:, M:].clone()
+    torch.cuda.synchronize()
+    ctx.dgemm(False, M, N, K, -1.0, A.data_ptr(), lda, B.data_ptr(), ldb, 1.0, C.data_ptr(), ldc)
+    torch.cuda.synchronize()
+    err = (C[:, :M].t() - ref).abs().max().item() / ref.abs().max().item()
+    assert err < 1e-14 * max(1.0, K ** 0.5), err
+    assert torch.equal(C[:, M:], keep)  # padding rows untouched
