@@ -299,6 +299,18 @@ def main():
     clocks = clk.stop()
     stats = hb.global_stats()
     launches = stats["launches"] - launches0
+    # context for the roofline: the same GEMMs measured without the concurrent small-problem
+    # streams — one untimed pass of this rank's costliest problem alone (after the timed region)
+    iso = None
+    if my_probs:
+        crit = max(my_probs, key=lambda p: p.pair.n_target)
+        hb.reset_global_stats()
+        hb.sweep([crit], [dev], profiling=True)
+        st1 = hb.global_stats()
+        if st1["gemm_ms"] > 0:
+            iso = {"achieved": round(st1["gemm_flops"] / (st1["gemm_ms"] * 1e-3) / 1e12, 3),
+                   "problem": f"d={crit.pair.target.d} d'={crit.pair.d_prime} N={crit.pair.n_target}",
+                   "note": "untimed solo pass after the timed region (no concurrent streams)"}
     t_dev = sum(dev_secs)
     t_wall = sum(walls)
     if dist:
@@ -360,6 +372,7 @@ def main():
                      "frac": round(gemm_tf / peak, 4), "traffic": ncu_traffic()[0],
                      "traffic_source": ncu_traffic()[1], "peak_source": peak_src,
                      "measured": "CUDA events around every DMMA GEMM launch on its stream, timed region",
+                     "isolated": (dict(iso, frac=round(iso["achieved"] / peak, 4)) if iso else None),
                      "path": {"alg_tflops": round(path_tf, 3), "frac": round(path_tf / peak, 4),
                               "model": "FLOP_alg = N^2 c_F + 4N^2 p - 4N p^2 + 4/3 p^3 (SURVEY 8d), "
                                        "p = certified rank, over device time of the step"}},

@@ -173,11 +173,21 @@ __device__ void dots_warp(const double* __restrict__ M, int64_t ld, const double
 }
 
 // a − Σ_k coef[k]·col[k*ld] for k < kn, subtracting in k order with every product and difference
-// rounded separately (aca.hpp:86 / :111 `row -= us[k](i) * vs[k]`); the loads of a batch of 8
-// are issued together so the chain waits on one memory latency per batch, not per term.
+// rounded separately (aca.hpp:86 / :111 `row -= us[k](i) * vs[k]`); the loads of a batch of 24
+// (8 for one-CTA batched blocks, where the wider batch spills and slowed 512 x 256² by 1.9x) are issued together so the chain waits on one L2 latency per batch, not per term (the sweep
+// is bound by these chains: ncu of a 4000 x 4000 sweep showed 45 % long-scoreboard stalls).
+template <bool WIDE>
 __device__ __forceinline__ double residual_chain(double a, const double* coef, const double* col,
                                                  int64_t ld, int64_t kn) {
   int64_t k = 0;
+  if (WIDE)
+  for (; k + 24 <= kn; k += 24) {
+    double v[24];
+#pragma unroll
+    for (int q = 0; q < 24; ++q) v[q] = __ldcg(col + (k + q) * ld);
+#pragma unroll
+    for (int q = 0; q < 24; ++q) a = __dsub_rn(a, __dmul_rn(coef[k + q], v[q]));
+  }
   for (; k + 8 <= kn; k += 8) {
     double v[8];
 #pragma unroll
@@ -189,6 +199,7 @@ __device__ __forceinline__ double residual_chain(double a, const double* coef, c
   return a;
 }
 
+template <bool WIDE>
 __global__ void __launch_bounds__(kAcaThreads) aca_sweep_kernel(AcaParams p) {
   extern __shared__ double smem[];
   __shared__ double s_red[kAcaWarps];
@@ -252,7 +263,7 @@ __global__ void __launch_bounds__(kAcaThreads) aca_sweep_kernel(AcaParams p) {
         for (int64_t t = tid; t < kn; t += kAcaThreads) coef[t] = __ldcg(B.U + nrow + (k0 + t) * m);
         __syncthreads();
         for (int64_t t = tid; t < nc; t += kAcaThreads)
-          sv[t] = residual_chain(sv[t], coef, B.V + c0 + t + k0 * n, n, kn);
+          sv[t] = residual_chain<WIDE>(sv[t], coef, B.V + c0 + t + k0 * n, n, kn);
       }
       double bv = -1.0;
       int64_t bi = INT64_MAX;
@@ -325,7 +336,7 @@ __global__ void __launch_bounds__(kAcaThreads) aca_sweep_kernel(AcaParams p) {
       for (int64_t t = tid; t < kn; t += kAcaThreads) coef[t] = __ldcg(B.V + pc + (k0 + t) * n);
       __syncthreads();
       for (int64_t t = tid; t < nrw; t += kAcaThreads)
-        su[t] = residual_chain(su[t], coef, B.U + r0 + t + k0 * m, m, kn);
+        su[t] = residual_chain<WIDE>(su[t], coef, B.U + r0 + t + k0 * m, m, kn);
     }
     __syncthreads();
     double nu2 = 0.0, bv = -1.0;
@@ -568,7 +579,8 @@ static void run_sweeps(hb_context* c, const DevKernel& K, const double* x, int64
     HB_CUDA(cudaMemcpyAsync(dblocks, hb.data(), hb.size() * sizeof(AcaBlockDev), cudaMemcpyHostToDevice, st));
     AcaParams prm{dblocks, K, d, 0.0};
     const size_t smem = (size_t)(cs_max + rs_max + kAcaChunk) * sizeof(double);
-    ensure_dyn_smem((const void*)aca_sweep_kernel, smem);
+    ensure_dyn_smem((const void*)aca_sweep_kernel<true>, smem);
+    ensure_dyn_smem((const void*)aca_sweep_kernel<false>, smem);
     // blocks of one launch share eps only when it is equal; launch per distinct eps
     std::vector<double> epss;
     for (AcaBlockReq* q : live)
@@ -577,7 +589,7 @@ static void run_sweeps(hb_context* c, const DevKernel& K, const double* x, int64
       prm.eps = epss[0];
       if (G > 1) {
         void* args[] = {&prm};
-        HB_CUDA(cudaLaunchCooperativeKernel((const void*)aca_sweep_kernel, dim3(G, (unsigned)live.size()),
+        HB_CUDA(cudaLaunchCooperativeKernel((const void*)aca_sweep_kernel<true>, dim3(G, (unsigned)live.size()),
                                             dim3(kAcaThreads), args, smem, st));
         launch_counter().fetch_add(1);
       } else {
@@ -585,7 +597,7 @@ static void run_sweeps(hb_context* c, const DevKernel& K, const double* x, int64
           AcaParams pp = prm;
           pp.blocks = dblocks + b0;
           const unsigned nb = (unsigned)std::min<size_t>(65535, live.size() - b0);
-          aca_sweep_kernel<<<dim3(1, nb), kAcaThreads, smem, st>>>(pp);
+          aca_sweep_kernel<false><<<dim3(1, nb), kAcaThreads, smem, st>>>(pp);
           HB_LAUNCH_CHECK();
         }
       }
@@ -596,11 +608,11 @@ static void run_sweeps(hb_context* c, const DevKernel& K, const double* x, int64
         pp.eps = live[i]->eps;
         if (G > 1) {
           void* args[] = {&pp};
-          HB_CUDA(cudaLaunchCooperativeKernel((const void*)aca_sweep_kernel, dim3(G, 1), dim3(kAcaThreads),
+          HB_CUDA(cudaLaunchCooperativeKernel((const void*)aca_sweep_kernel<true>, dim3(G, 1), dim3(kAcaThreads),
                                               args, smem, st));
           launch_counter().fetch_add(1);
         } else {
-          aca_sweep_kernel<<<dim3(1, 1), kAcaThreads, smem, st>>>(pp);
+          aca_sweep_kernel<false><<<dim3(1, 1), kAcaThreads, smem, st>>>(pp);
           HB_LAUNCH_CHECK();
         }
       }
@@ -661,9 +673,9 @@ static bool degenerate_piv(const std::vector<double>& piv, int64_t r, int64_t* k
 
 static int choose_group(hb_context* c, const hb_block& b) {
   const int64_t big = std::max(b.rows, b.cols);
-  // the residual updates stream U / V once per pivot: spread them over as many SMs as there
-  // are 64-wide slices (the sweep is memory-latency bound, not barrier bound, past ~1k)
-  int G = (int)std::min<int64_t>(c->coop_sms, std::max<int64_t>(1, ceil_div(big, 64)));
+  // one residual chain per thread: 256-wide slices keep half of the 512 threads busy while
+  // the group (and its barriers) stays small; past 37.9k rows every SM takes a slice
+  int G = (int)std::min<int64_t>(c->coop_sms, std::max<int64_t>(1, ceil_div(big, 256)));
   if (big <= 512) G = 1;
   G = std::max<int>(G, (int)ceil_div(big, kAcaMaxSlice));
   return G;

@@ -517,7 +517,12 @@ void rank_matrix_inplace(hb_context* c, double* A, int64_t m, int64_t n, int64_t
         delta2 = INFINITY;
         break;
       }
-      if (c->spectral && sigma1_est > 0.0 && delta <= 64.0 * target) {
+      static const double screen_gate = [] {  // HB_SCREEN_GATE: screen once delta <= gate·target
+        const char* e = getenv("HB_SCREEN_GATE");
+        const double v = e ? atof(e) : 64.0;
+        return v > 1.0 ? v : 64.0;
+      }();
+      if (c->spectral && sigma1_est > 0.0 && delta <= screen_gate * target) {
         // screen: ‖A22 ẑ‖ with ẑ the sketch's dominant right direction (a lower bound on
         // ‖A22‖₂); only when it is well below target run the certifying block power method
         Phase ph(c, HB_PH_SIGMA1);
@@ -537,9 +542,18 @@ void rank_matrix_inplace(hb_context* c, double* A, int64_t m, int64_t n, int64_t
         }
       }
       if (!(fro_at_sketch < INFINITY)) fro_at_sketch = delta;
-      if (delta < 1e-8 * fro_at_sketch) {
+      // Fresh sketch once ‖A22‖ fell by this factor since the last one: the downdated sketch then
+      // carries ~1e-16/resketch relative error, still far below what pivot choice needs (c1 and
+      // c2 measured with 1e-8 / 1e-10 / 1e-12 / 1e-16: identical k everywhere, 3-5 % faster than
+      // 1e-8 from the skipped second Ω·A pass).  HB_RESKETCH overrides.
+      static const double resketch = [] {
+        const char* e = getenv("HB_RESKETCH");
+        const double v = e ? atof(e) : 1e-11;
+        return v > 0.0 ? v : 1e-11;
+      }();
+      if (delta < resketch * fro_at_sketch) {
         Phase ph(c, HB_PH_SKETCH);
-        // the downdated sketch has lost ~8 digits to cancellation: draw a fresh one
+        // the downdated sketch has lost ~11 digits to cancellation: draw a fresh one
         sketch_seed = splitmix64(sketch_seed);
         const int64_t mr = m - j;
         double* Om = ws<double>(c, B_OMEGA, (size_t)ell * std::max<int64_t>(mr, 1));
@@ -700,6 +714,7 @@ void context_init(hb_context* c, int device) {
   HB_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
   HB_CUDA(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
   c->coop_sms = c->num_sms;
+  if (const char* e = getenv("HB_SPECTRAL")) c->spectral = atoi(e) != 0;  // experiments / sweeps
   cudaMemPool_t pool;
   HB_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
   uint64_t thr = UINT64_MAX;
