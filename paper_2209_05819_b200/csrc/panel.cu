@@ -23,7 +23,6 @@ __global__ void __launch_bounds__(kPanelThreads) panel_qr_smem_kernel(PanelParam
   constexpr int NW = kPanelThreads / 32;
   extern __shared__ double psm[];
   __shared__ double red[NW][128];
-  __shared__ double sh[3];
   const int G = gridDim.x, g = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int b = p.b;
@@ -33,7 +32,6 @@ __global__ void __launch_bounds__(kPanelThreads) panel_qr_smem_kernel(PanelParam
   const int ldS = (int)chunk + 1;        // odd stride: column-wise and row-wise smem access both spread
   double* S = psm;                       // [b][ldS]
   double* ws = psm + (size_t)b * ldS;    // [b]  w_q
-  double* gs = ws + b;                   // [b]  reduced g_q
   double* P = p.P;
   const int64_t ld = p.ld;
   const int nref = (int)min((int64_t)b, p.mp);
@@ -77,43 +75,52 @@ __global__ void __launch_bounds__(kPanelThreads) panel_qr_smem_kernel(PanelParam
       for (int j = 0; j < 4; ++j) red[warp][lane + 32 * j] = s[j];
     }
     __syncthreads();
-    if (tid < b - c) {
+    // every thread forms the reflector itself from the reduced g_c (same arithmetic, same order:
+    // identical in all threads and CTAs) — no extra barrier for a broadcast
+    double gc = 0.0;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) gc += red[w][0];
+    const double alpha = __ldcg(rc + c);
+    double tau = 0.0, scal = 0.0, beta = alpha;
+    if (gc > 0.0) {
+      beta = -copysign(sqrt(alpha * alpha + gc), alpha);
+      tau = (beta - alpha) / beta;
+      scal = 1.0 / (alpha - beta);
+    }
+    if (g == 0 && tid == 0) p.tau[c] = tau;
+    for (int q = c + 1 + tid; q < b; q += kPanelThreads) {
       double t = 0.0;
 #pragma unroll
-      for (int w = 0; w < NW; ++w) t += red[w][tid];
-      gs[c + tid] = t;
+      for (int w = 0; w < NW; ++w) t += red[w][q - c];
+      ws[q] = tau * (__ldcg(rc + q) + scal * t);
     }
-    __syncthreads();
-    if (tid == 0) {
-      const double alpha = __ldcg(rc + c), s = gs[c];
-      double tau = 0.0, scal = 0.0, beta = alpha;
-      if (s > 0.0) {
-        beta = -copysign(sqrt(alpha * alpha + s), alpha);
-        tau = (beta - alpha) / beta;
-        scal = 1.0 / (alpha - beta);
-      }
-      sh[0] = tau; sh[1] = scal; sh[2] = beta;
-      if (g == 0) p.tau[c] = tau;
-    }
-    __syncthreads();
-    const double tau = sh[0], scal = sh[1];
-    for (int q = c + 1 + tid; q < b; q += kPanelThreads) ws[q] = tau * (__ldcg(rc + q) + scal * gs[q]);
     const int ic = (int)max((int64_t)0, (int64_t)c - r0);        // first local row >= c
     const int i1 = (int)max((int64_t)0, (int64_t)(c + 1) - r0);  // first local row > c
     const int in = (int)max((int64_t)0, (int64_t)(c + 2) - r0);  // first local row > c+1
     double* Sc = S + c * ldS;
-    for (int i = i1 + tid; i < rows; i += kPanelThreads) Sc[i] *= scal;
-    if (ic < i1 && ic < rows && tid == 0) Sc[ic] = sh[2];  // row c: R diagonal (v_c = 1 implicit)
-    __syncthreads();
-    if (c + 1 >= b) break;
-    // ---- column c+1 first (its entries feed the partials of the other columns) ----
-    {
+    // scale v (column c) and, in the same pass and thread→row mapping, update column c+1 (its
+    // entries feed the partials of the other columns); w_{c+1} is formed by every thread
+    if (c + 1 < b) {
+      double t1 = 0.0;
+#pragma unroll
+      for (int w = 0; w < NW; ++w) t1 += red[w][1];
+      const double wq = tau * (__ldcg(rc + c + 1) + scal * t1);  // == ws[c+1]
       double* Sq = S + (c + 1) * ldS;
-      const double wq = ws[c + 1];
-      if (ic < i1 && ic < rows && tid == 0) Sq[ic] -= wq;
-      for (int i = i1 + tid; i < rows; i += kPanelThreads) Sq[i] = fma(-Sc[i], wq, Sq[i]);
+      for (int i = i1 + tid; i < rows; i += kPanelThreads) {
+        const double v = Sc[i] * scal;
+        Sc[i] = v;
+        Sq[i] = fma(-v, wq, Sq[i]);
+      }
+      if (ic < i1 && ic < rows && tid == 0) {  // row c: R diagonal (v_c = 1 implicit)
+        Sc[ic] = beta;
+        Sq[ic] -= wq;
+      }
+    } else {
+      for (int i = i1 + tid; i < rows; i += kPanelThreads) Sc[i] *= scal;
+      if (ic < i1 && ic < rows && tid == 0) Sc[ic] = beta;
     }
     __syncthreads();
+    if (c + 1 >= b) break;
     const bool more = c + 1 < nref;
     double* pn = part + (size_t)(par ^ 1) * G * b;
     double* rn = rowc + (par ^ 1) * b;

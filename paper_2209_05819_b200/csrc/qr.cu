@@ -272,7 +272,9 @@ __global__ void __launch_bounds__(kSketchThreads) sketch_cpqr_smem_kernel(Sketch
   __shared__ double wbest[NW], wsum[NW];
   __shared__ int wbi[NW];
   __shared__ double sh_tau;
-  __shared__ int sh_piv, sh_stop, sh_win;
+  __shared__ int sh_win;
+  __shared__ int wh[NW];
+  int piv_r = 0, win_r = 0, stop_r = 0;
 
   double best = -1.0, sum = 0.0;
   int bi = INT_MAX;
@@ -334,31 +336,30 @@ __global__ void __launch_bounds__(kSketchThreads) sketch_cpqr_smem_kernel(Sketch
         if (better(ob, oi, b0, i0)) { b0 = ob; i0 = oi; h0 = oh; }
       }
       s0 = warp_sum(s0);
-      if (lane == 0) { wbest[warp] = b0; wbi[warp] = i0; wsum[warp] = s0; v[warp] = (double)h0; }
+      if (lane == 0) { wbest[warp] = b0; wbi[warp] = i0; wsum[warp] = s0; wh[warp] = h0; }
       __syncthreads();
-      if (tid == 0) {
-        double bb = -1.0, ss = 0.0;
-        int ii = INT_MAX, hh = -1;
-        for (int w = 0; w < NW; ++w) {
-          if (better(wbest[w], wbi[w], bb, ii)) { bb = wbest[w]; ii = wbi[w]; hh = (int)v[w]; }
-          ss += wsum[w];
-        }
-        const double est = c < ell ? ss / (double)(ell - c) : 0.0;
-        if (g == 0) p.out_est[c] = est;
-        int stop = 0;
-        if (!(bb > 0.0) || c >= ell) stop = 1;
-        else if (c >= p.b_min && (c % 8) == 0 && est <= p.stop_fro2) stop = 1;
-        sh_stop = stop;
-        sh_piv = ii;
-        sh_win = hh;
+      // every thread combines the NW warp results itself (same order: identical decisions), so
+      // no second barrier is needed to broadcast them
+      double bb = -1.0, ss = 0.0;
+      int ii = INT_MAX, hh = -1;
+      for (int w = 0; w < NW; ++w) {
+        if (better(wbest[w], wbi[w], bb, ii)) { bb = wbest[w]; ii = wbi[w]; hh = wh[w]; }
+        ss += wsum[w];
       }
-      __syncthreads();
+      const double est = c < ell ? ss / (double)(ell - c) : 0.0;
+      if (g == 0 && tid == 0) p.out_est[c] = est;
+      int stop = 0;
+      if (!(bb > 0.0) || c >= ell) stop = 1;
+      else if (c >= p.b_min && (c % 8) == 0 && est <= p.stop_fro2) stop = 1;
+      piv_r = ii;
+      win_r = hh;
+      stop_r = stop;
     }
-    if (sh_stop) break;
-    const int piv = sh_piv;
+    if (stop_r) break;
+    const int piv = piv_r;
     // Householder vector of the winner's column (rows c..ell-1), redundantly in every CTA
     if (warp == 0) {
-      const double* col = p.cand + ((size_t)par * G + sh_win) * ell;
+      const double* col = p.cand + ((size_t)par * G + win_r) * ell;
       double yv[RPL];
       double s = 0.0;
 #pragma unroll
