@@ -26,6 +26,7 @@ struct SketchParams {
 };
 
 constexpr int kPanelThreads = 512;  // panel_qr_smem_kernel block size
+constexpr size_t kPanelClusterSmem = 220 * 1024;  // per-CTA budget of the cluster panel kernel
 
 struct PanelParams {
   double* P;  // panel (mp x b), column-major
@@ -41,6 +42,10 @@ struct PanelParams {
   double* scal;    // [2] published alpha (shared-memory panel kernel)
   GridBarrier bar;
 };
+
+size_t panel_cluster_smem(int64_t chunk, int b, int G);
+int panel_cluster_max();
+void launch_panel_cluster(const PanelParams& pp, int G, cudaStream_t st);
 
 struct PowerParams {
   const double* R;  // rows 0..b-1 of the factor

@@ -110,6 +110,29 @@ void panel_and_T(hb_context* c, double* P, int64_t ld, int64_t mp, int b, double
   };
   const int G = panel_ctas(mp, b);
   const int64_t chunk = ceil_div(mp, G);
+  // whole panel in one cluster's distributed shared memory: DSMEM exchange + hardware cluster
+  // barrier per column instead of L2 partials + a grid barrier (HB_PANEL_CLUSTER=0 disables)
+  static const bool cluster_on = [] {
+    const char* e = getenv("HB_PANEL_CLUSTER");
+    return !(e && atoi(e) == 0);
+  }();
+  if (cluster_on && b > 0) {
+    const int cmax = panel_cluster_max();
+    int Gc = (int)std::max<int64_t>(2, ceil_div(mp * b * 8, 150 * 1024));
+    if (cmax > 0 && Gc <= cmax) {
+      while (Gc < cmax && panel_cluster_smem(ceil_div(mp, Gc), b, Gc) > kPanelClusterSmem) ++Gc;
+      if (Gc > 8 && cmax == 16) Gc = 16;  // cluster sizes 2..8 portable, 16 opt-in
+      const int64_t chc = ceil_div(mp, Gc);
+      if (panel_cluster_smem(chc, b, Gc) <= kPanelClusterSmem) {
+        PanelParams pp{};
+        pp.P = P; pp.ld = ld; pp.mp = mp; pp.b = b; pp.chunk = chc;
+        pp.tau = tau; pp.V = V; pp.ldv = ldv;
+        launch_panel_cluster(pp, Gc, st);
+        build_T(c, V, ldv, mp, b, tau, T, B_S);
+        return;
+      }
+    }
+  }
   const int64_t budget = (200 * 1024) / 8;  // doubles of shared memory per CTA
   int bsub = (int)std::min<int64_t>(b, budget / (chunk + 3));
   if (bsub >= 8 && bsub < b) bsub &= ~7;
