@@ -321,36 +321,41 @@ __global__ void __launch_bounds__(kPanelThreads) panel_qr_cluster_kernel(PanelPa
 
 namespace hb {
 
-// Largest cluster size the panel kernel can launch with at the full shared-memory budget (16
-// needs the non-portable opt-in; 0 = no cluster launch possible).
-int panel_cluster_max() {
-  static int cap = -1;
-  if (cap >= 0) return cap;
-  cap = 0;
+int cluster_cap(const void* kern, int threads, size_t smem) {
+  static std::mutex mu;
+  static std::map<const void*, int> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find(kern);
+  if (it != cache.end()) return it->second;
+  int cap = 0;
   for (int G : {16, 8}) {
-    if (G == 16 && cudaFuncSetAttribute((const void*)panel_qr_cluster_kernel,
-                                        cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
+    if (G == 16 && cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
       cudaGetLastError();
       continue;
     }
-    const size_t smem = kPanelClusterSmem;
-    ensure_dyn_smem((const void*)panel_qr_cluster_kernel, smem);
+    ensure_dyn_smem(kern, smem);
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(G);
-    cfg.blockDim = dim3(kPanelThreads);
+    cfg.blockDim = dim3(threads);
     cfg.dynamicSmemBytes = smem;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = G; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
     cfg.attrs = at; cfg.numAttrs = 1;
     int n = 0;
-    if (cudaOccupancyMaxActiveClusters(&n, (const void*)panel_qr_cluster_kernel, &cfg) == cudaSuccess && n > 0) {
+    if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) == cudaSuccess && n > 0) {
       cap = G;
       break;
     }
     cudaGetLastError();
   }
+  cache[kern] = cap;
   return cap;
+}
+
+// Largest cluster size the panel kernel can launch with at the full shared-memory budget.
+int panel_cluster_max() {
+  return cluster_cap((const void*)panel_qr_cluster_kernel, kPanelThreads, kPanelClusterSmem);
 }
 
 void launch_panel_cluster(const PanelParams& pp, int G, cudaStream_t st) {

@@ -44,6 +44,9 @@ struct PanelParams {
 };
 
 size_t panel_cluster_smem(int64_t chunk, int b, int G);
+// Largest cluster (16 with the non-portable opt-in, else 8, else 0) `kern` can launch with at
+// `threads` threads and `smem` bytes of dynamic shared memory per CTA (cached per kernel).
+int cluster_cap(const void* kern, int threads, size_t smem);
 int panel_cluster_max();
 void launch_panel_cluster(const PanelParams& pp, int G, cudaStream_t st);
 
