@@ -170,18 +170,34 @@ class ClockSampler:
 
 
 def cpu_baseline_run(wl_sample, threads: int):
-    """Oracle (C assembly + LAPACK gesdd) on a bounded sample: entries/s on the host cores."""
+    """The reference's CPU path on a bounded sample: entries/s on the host cores.  Assembly is
+    the reference's own hodlr::assemble_dense (kernel.hpp:168-181, serial as written) compiled
+    from /root/reference into oracle/_ref when that library is present, else the oracle's C
+    restatement on all threads; the ε-rank is LAPACK gesdd on all threads (SPEC epsilon_rank —
+    the reference has no rank driver in code).  Returns (G/s, s, entries, kind)."""
     os.environ.setdefault("OPENBLAS_NUM_THREADS", str(threads))
     from oracle import oracle as O
     O.build()
+    use_ref = O.ref_available()
     t0 = time.perf_counter()
     ent = 0
     for (d, dp, k, n, tols) in wl_sample:
         seed = O.problem_seed(0, d, dp, n)
-        O.rank_problem(d, dp, k, n, tols, seed=seed, nthreads=threads)
+        x, y = O.pair_points(d, dp, n, O.UNIFORM, seed)
+        if use_ref:
+            K = O.ref_assemble(O.KERNEL_IDS[k], x, y)
+        else:
+            K = O.assemble(O.KERNEL_IDS[k], x, y, nthreads=threads)
+        s = O.singular_values(K)
+        [O.epsilon_rank_from_sigma(s, t) for t in tols]
         ent += n * n
     dt = time.perf_counter() - t0
-    return ent / dt / 1e9, dt, ent
+    return ent / dt / 1e9, dt, ent, ("reference" if use_ref else "port")
+
+
+def _assembly_desc(kind: str, threads: int) -> str:
+    return ("the reference's assemble_dense (kernel.hpp, compiled in oracle/_ref), serial"
+            if kind == "reference" else f"oracle C assembly on {threads} threads")
 
 
 def golden_map():
@@ -236,8 +252,9 @@ def main():
         for _ in range(args.warmup):
             cpu_baseline_run(sample[:3], threads)
         vals, dts = [], []
+        kind = "port"
         for _ in range(args.steps):
-            v, dt, ent = cpu_baseline_run(sample, threads)
+            v, dt, ent, kind = cpu_baseline_run(sample, threads)
             vals.append(v)
             dts.append(dt)
         v = statistics.median(vals)
@@ -248,9 +265,10 @@ def main():
                 "dtype": "f64", "data": "synthetic",
                 "config": cfg,
                 "cpu_baseline": {"value": round(v, 6), "unit": "G entries/s", "cores": threads,
-                                 "kind": "port",
+                                 "kind": kind,
                                  "sample": f"{len(sample)} workload problems with N <= "
-                                           f"{args.cpu_sample_max_n} (oracle C assembly + numpy/LAPACK gesdd)"},
+                                           f"{args.cpu_sample_max_n} ({_assembly_desc(kind, threads)} "
+                                           f"+ numpy/LAPACK gesdd on {threads} threads)"},
                 "e2e": {"value": round(v, 6), "unit": "G entries/s", "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)
@@ -387,12 +405,12 @@ def main():
         "gemm_ms": round(stats["gemm_ms"], 1),
     }
     if world == 1 and not args.no_cpu_baseline:
-        v, dt, ent = cpu_baseline_run(sample, threads)
+        v, dt, ent, kind = cpu_baseline_run(sample, threads)
         line["cpu_baseline"] = {"value": round(v, 6), "unit": "G entries/s", "cores": threads,
-                                "kind": "port",
+                                "kind": kind,
                                 "sample": f"{len(sample)} workload problems with N <= "
-                                          f"{args.cpu_sample_max_n} ({dt:.1f} s; oracle C assembly on "
-                                          f"{threads} threads + numpy/LAPACK gesdd)"}
+                                          f"{args.cpu_sample_max_n} ({dt:.1f} s; {_assembly_desc(kind, threads)} "
+                                          f"+ numpy/LAPACK gesdd on {threads} threads)"}
     if args.details:
         Path(args.details).write_text(json.dumps({
             "results": [[r.__dict__ for r in res] for res in full], "workload": wl,
