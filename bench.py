@@ -129,7 +129,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", "100"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -139,6 +139,15 @@ class ClockSampler:
     def _read(self):
         for line in self.proc.stdout:
             self.lines.append(line.strip())
+
+    def wait_first(self, timeout: float = 15.0):
+        """nvidia-smi's start-up (NVML load, first query) costs host CPU for up to seconds on a
+        fresh box; wait for its first sample so that cost lands before the timed region (host
+        round trips of the sweep driver are inside the device-timed span)."""
+        t0 = time.perf_counter()
+        while self.proc and not self.lines and time.perf_counter() - t0 < timeout:
+            time.sleep(0.02)
+        self.skip = len(self.lines)
 
     def stop(self) -> dict:
         if not self.proc:
@@ -151,7 +160,7 @@ class ClockSampler:
         self.t.join(timeout=2)
         sm, smax, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        for ln in self.lines[getattr(self, "skip", 0):] or self.lines[-1:]:
             f = [x.strip() for x in ln.split(",")]
             if len(f) < 9:
                 continue
@@ -210,7 +219,7 @@ def golden_map():
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c1", choices=["c0", "c1", "c2", "c3", "sweep"],
@@ -299,12 +308,13 @@ def main():
             dist.barrier(device_ids=[dev])
         torch.cuda.synchronize()
 
+    clk = ClockSampler(dev)
+    clk.start()
+    clk.wait_first()
     for _ in range(args.warmup):
         hb.sweep(my_probs, [dev])
     hb.reset_global_stats()
     launches0 = hb.global_stats()["launches"]
-    clk = ClockSampler(dev)
-    clk.start()
     barrier()
     dev_secs, walls, my_res, statuses = [], [], None, []
     for _ in range(args.steps):

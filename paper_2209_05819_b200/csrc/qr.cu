@@ -845,29 +845,41 @@ __global__ void transpose_upper_kernel(const double* __restrict__ A, int64_t lda
 __global__ void __launch_bounds__(256) gram_sigma1_kernel(const double* __restrict__ G, int b, int iters,
                                                           double* __restrict__ out) {
   extern __shared__ double gs[];  // b x b
-  __shared__ double x[kSketchRows], y[kSketchRows], red[32];
-  const int tid = threadIdx.x;
+  __shared__ double x[kSketchRows], y[kSketchRows], part[2][kSketchRows], red[3][8];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int e = tid; e < b * b; e += blockDim.x) gs[e] = G[e];
   for (int i = tid; i < b; i += blockDim.x) x[i] = 1.0;
   __syncthreads();
+  // thread (i, h): half h of row i's dot product (b <= 128 rows x 2 halves = 256 threads), so
+  // the dependent FMA chain is b/2 long; the three reductions share one pass
+  const int i = tid % kSketchRows, h = tid / kSketchRows;
+  const int j0 = h * ((b + 1) / 2), j1 = h ? b : (b + 1) / 2;
   double best = 0.0;
   for (int it = 0; it < iters; ++it) {
-    double xx = 0.0, xy = 0.0;
-    for (int i = tid; i < b; i += blockDim.x) {
+    if (i < b) {
       double s = 0.0;
-      for (int j = 0; j < b; ++j) s = fma(gs[i + j * b], x[j], s);  // G symmetric: row i = column i
-      y[i] = s;
-      xx += x[i] * x[i];
-      xy += x[i] * s;
+      for (int j = j0; j < j1; ++j) s = fma(gs[i + j * b], x[j], s);  // G symmetric: row i = column i
+      part[h][i] = s;
     }
-    xx = block_sum(xx, red);
-    xy = block_sum(xy, red);
+    __syncthreads();
+    double xx = 0.0, xy = 0.0, yy = 0.0;
+    if (h == 0 && i < b) {
+      const double s = part[0][i] + part[1][i];
+      y[i] = s;
+      xx = x[i] * x[i];
+      xy = x[i] * s;
+      yy = s * s;
+    }
+    xx = warp_sum(xx);
+    xy = warp_sum(xy);
+    yy = warp_sum(yy);
+    if (lane == 0) { red[0][warp] = xx; red[1][warp] = xy; red[2][warp] = yy; }
+    __syncthreads();
+    xx = 0.0; xy = 0.0; yy = 0.0;
+    for (int w = 0; w < 8; ++w) { xx += red[0][w]; xy += red[1][w]; yy += red[2][w]; }
     if (xx > 0.0) best = fmax(best, xy / xx);
-    double yy = 0.0;
-    for (int i = tid; i < b; i += blockDim.x) yy += y[i] * y[i];
-    yy = block_sum(yy, red);
     const double sc = yy > 0.0 ? 1.0 / sqrt(yy) : 0.0;
-    for (int i = tid; i < b; i += blockDim.x) x[i] = y[i] * sc;
+    if (h == 0 && i < b) x[i] = y[i] * sc;
     __syncthreads();
   }
   if (tid == 0) *out = sqrt(fmax(best, 0.0));
