@@ -16,6 +16,8 @@
  *   hb_eval_radial_host    <- hodlr::eval_radial (scalar, host)     kernel.hpp:149-157
  *   hb_rank_matrix         <- SPEC epsilon_rank(matrix, epsilon)
  *   hb_rank                <- SPEC pair_geometry -> assemble_dense -> epsilon_rank
+ *   hb_rank_complex        <- the paper's complex F3 / F4 tables from the
+ *                             reference's real/imaginary kernel pairs (kernel.hpp:22-27)
  *   hb_sweep               <- SPEC rank_table + parallel_for        SPEC.md:570-578, parallel.hpp:12-29
  *   hb_block               <- hodlr::BlockSpec index ranges         aca.hpp:16-28
  *   hb_aca_factor          <- hodlr::ACAFactor                      aca.hpp:50-62
@@ -159,6 +161,16 @@ hb_status hb_rank_matrix(hb_context* ctx, const double* d_A, int64_t m, int64_t 
 /* k1 + k2 + k3: generate, assemble and rank one pair (out has ntol entries). */
 hb_status hb_rank(hb_context* ctx, const hb_kernel* kernel, const hb_pair* pair,
                   const double* tols, int32_t ntol, hb_rank_result* out);
+
+/* ε-rank of the complex block K_re + i·K_im — the paper's F3 = e^{ir}/r (HB_K_HELMHOLTZ3D_RE/IM)
+ * and F4 = H_2^(1)(r) (HB_K_HANKEL_H12_RE/IM) columns; the reference exposes
+ * their real and imaginary parts as separate real kernels (kernel.hpp:22-27).  Computed through
+ * the real 2m x 2n embedding [[Re, −Im], [Im, Re]], whose singular values are those of K, each
+ * twice: rank = count/2; an odd count (a σ pair straddling the threshold) leaves the bracket open
+ * (certificate 0).  k_factored and hb_last_sigma refer to the embedding. */
+hb_status hb_rank_complex(hb_context* ctx, const hb_kernel* kernel_re, const hb_kernel* kernel_im,
+                          const hb_pair* pair, const double* tols, int32_t ntol,
+                          hb_rank_result* out);
 
 /* Singular values (descending) of R_k from the last certification on this context.
  * Copies min(max, count) values to host_out; *count = number available. */

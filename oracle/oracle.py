@@ -182,6 +182,22 @@ def rank_problem(d: int, dprime: int | None, kernel: str, n: int, tols, mode: in
     return [epsilon_rank_from_sigma(s, t) for t in tols]
 
 
+def rank_problem_complex(d: int, dprime: int | None, kernel_re: str, kernel_im: str, n: int, tols,
+                         mode: int = UNIFORM, seed: int = 0, nthreads: int = None) -> list[RankRecord]:
+    """ε-rank of K_re + i·K_im (the paper's complex F3 = e^{ir}/r and F4 = H_2^(1)(r) columns,
+    PAPER.md:121-131, from the reference's real/imaginary kernel pairs kernel.hpp:22-27) with
+    numpy's complex LAPACK SVD (zgesdd)."""
+    nthreads = nthreads or os.cpu_count() or 1
+    x, y = pair_points(d, dprime, n, mode, seed)
+    A = assemble(KERNEL_IDS[kernel_re], x, y, nthreads=nthreads)
+    B = assemble(KERNEL_IDS[kernel_im], x, y, nthreads=nthreads)
+    s = singular_values(A + 1j * B)
+    return [epsilon_rank_from_sigma(s, t) for t in tols]
+
+
+COMPLEX_COLUMNS = {"F3": ("helmholtz3d_re", "helmholtz3d_im"), "F4": ("hankel_h12_re", "hankel_h12_im")}
+
+
 # ---- ACA (aca.hpp:16-213) and the compiled reference (oracle/_ref) -----------------------------
 REF_LIB = HERE / "_ref" / "libhb_ref.so"
 _ref = None

@@ -106,6 +106,18 @@ __global__ void __launch_bounds__(256) assemble_kernel(const double* __restrict_
   if (bad) atomicOr(flags, bad);
 }
 
+__global__ void negate_block_kernel(double* __restrict__ A, int64_t m, int64_t n, int64_t ld) {
+  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= m * n) return;
+  const int64_t i = idx % m, j = idx / m;
+  A[i + j * ld] = -A[i + j * ld];
+}
+
+void launch_negate(double* A, int64_t m, int64_t n, int64_t ld, cudaStream_t st) {
+  negate_block_kernel<<<(unsigned)ceil_div(m * n, 256), 256, 0, st>>>(A, m, n, ld);
+  HB_LAUNCH_CHECK();
+}
+
 void launch_points(const hb_cube& cube, int64_t n, int mode, int64_t m_axis, uint64_t seed,
                    int role, double* out, cudaStream_t st) {
   const int64_t total = n * cube.d;

@@ -14,6 +14,7 @@ struct GridBarrier;
 void launch_points(const hb_cube& cube, int64_t n, int mode, int64_t m_axis, uint64_t seed,
                    int role, double* out, cudaStream_t st);
 bool kernel_singular_at_origin(int id);
+void launch_negate(double* A, int64_t m, int64_t n, int64_t ld, cudaStream_t st);
 void launch_assemble(const hb_kernel& kern, const double* x, int64_t T, const double* y,
                      int64_t N, int d, double* K, int64_t ldk, unsigned int* flags,
                      cudaStream_t st);

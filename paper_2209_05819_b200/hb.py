@@ -107,7 +107,7 @@ EXPORTS = [
     "hb_version", "hb_status_string", "hb_last_error", "hb_context_create", "hb_context_destroy",
     "hb_context_stream", "hb_context_set_tuning", "hb_generate_points", "hb_assemble",
     "hb_eval_radial_host", "hb_rank_matrix", "hb_rank", "hb_last_sigma", "hb_sweep",
-    "hb_partition", "hb_problem_seed", "hb_phase_name", "hb_context_set_profiling",
+    "hb_partition", "hb_problem_seed", "hb_rank_complex", "hb_phase_name", "hb_context_set_profiling",
     "hb_stats_get", "hb_stats_reset", "hb_sweep_ex", "hb_sweep_release", "hb_context_set_stopping",
     # include/hb_debug.h (test hooks)
     "hb_debug_dgemm", "hb_debug_dgemm_async",
@@ -154,6 +154,10 @@ def load(path: os.PathLike | str | None = None):
     L.hb_rank.argtypes = [c_p, ctypes.POINTER(hb_kernel), ctypes.POINTER(hb_pair),
                           ctypes.POINTER(ctypes.c_double), ctypes.c_int32,
                           ctypes.POINTER(hb_rank_result)]
+    L.hb_rank_complex.argtypes = [c_p, ctypes.POINTER(hb_kernel), ctypes.POINTER(hb_kernel),
+                                  ctypes.POINTER(hb_pair), ctypes.POINTER(ctypes.c_double),
+                                  ctypes.c_int32, ctypes.POINTER(hb_rank_result)]
+    L.hb_rank_complex.restype = ctypes.c_int
     L.hb_last_sigma.argtypes = [c_p, ctypes.POINTER(ctypes.c_double), ctypes.c_int64,
                                 ctypes.POINTER(ctypes.c_int64)]
     L.hb_sweep.argtypes = [ctypes.POINTER(hb_problem), ctypes.c_int64,
@@ -349,6 +353,16 @@ class Context:
         out = (hb_rank_result * nt)()
         _check(self._lib.hb_rank(self._h, ctypes.byref(kernel), ctypes.byref(pair), ct, nt, out),
                "hb_rank", self._h)
+        return [RankResult.of(o) for o in out]
+
+    def rank_complex(self, kernel_re: hb_kernel, kernel_im: hb_kernel, pair: hb_pair,
+                     tols: Sequence[float]) -> list[RankResult]:
+        """ε-rank of K_re + i·K_im (the paper's complex F3 / F4 kernels) via the real embedding."""
+        nt = len(tols)
+        ct = (ctypes.c_double * nt)(*tols)
+        out = (hb_rank_result * nt)()
+        _check(self._lib.hb_rank_complex(self._h, ctypes.byref(kernel_re), ctypes.byref(kernel_im),
+                                         ctypes.byref(pair), ct, nt, out), "hb_rank_complex", self._h)
         return [RankResult.of(o) for o in out]
 
     def rank_matrix(self, d_A: int, m: int, n: int, ld: int, tols: Sequence[float]):

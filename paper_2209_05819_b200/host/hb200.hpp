@@ -249,6 +249,29 @@ inline std::vector<RankRecord> epsilon_rank(Device& dev, const KernelSpec& k, co
   return recs;
 }
 
+// ε-rank of the complex block K_re + i·K_im (the paper's F3 / F4 columns, PAPER.md:121-131;
+// e.g. Helmholtz3DReal + i·Helmholtz3DImag = e^{ir}/r, HankelH12Real + i·HankelH12Imag = H_2^(1)).
+inline std::vector<RankRecord> epsilon_rank_complex(Device& dev, const KernelSpec& re, const KernelSpec& im,
+                                                    const PairGeometry& g, const std::vector<double>& eps) {
+  if (eps.empty() || eps.size() > HB_MAX_TOLS) throw std::invalid_argument("need 1..4 tolerances");
+  const hb_kernel cr = re.to_c(), ci = im.to_c();
+  const hb_pair cp = g.to_c();
+  std::vector<hb_rank_result> out(eps.size());
+  check(hb_rank_complex(dev.get(), &cr, &ci, &cp, eps.data(), (int32_t)eps.size(), out.data()),
+        "epsilon_rank_complex", dev.get());
+  std::vector<RankRecord> recs;
+  for (size_t t = 0; t < eps.size(); ++t) {
+    RankRecord r;
+    r.kernel = kernel_name(re) + "+i*" + kernel_name(im); r.d = g.d; r.interaction = g.interaction;
+    r.N = g.n; r.epsilon = eps[t]; r.rank = out[t].rank; r.rank_lo = out[t].rank_lo;
+    r.rank_hi = out[t].rank_hi; r.k_factored = out[t].k_factored; r.sigma1 = out[t].sigma1;
+    r.sigma_r = out[t].sigma_r; r.sigma_r1 = out[t].sigma_r1; r.gap = out[t].gap;
+    r.seconds = out[t].sec[3];
+    recs.push_back(r);
+  }
+  return recs;
+}
+
 // SPEC epsilon_rank(matrix, epsilon) on a device matrix (column-major m x n, leading dim ld).
 inline int epsilon_rank(Device& dev, const double* d_matrix, int64_t m, int64_t n, int64_t ld,
                         double eps) {

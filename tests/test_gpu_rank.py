@@ -110,6 +110,39 @@ def test_paper_tables_small_n(ctx, hb, paper_tables):
     assert not bad, bad
 
 
+def test_paper_tables_complex_columns(ctx, hb, paper_tables):
+    """The complex F3 = e^{ir}/r and F4 = H_2^(1)(r) columns (real embedding, hb_rank_complex):
+    every table entry with N <= 5000, exact."""
+    cols = {"F3": ("helmholtz3d_re", "helmholtz3d_im"), "F4": ("hankel_h12_re", "hankel_h12_im")}
+    bad, n_cases = [], 0
+    for tab in paper_tables:
+        for row in tab["rows"]:
+            if row["N"] > 5000:
+                continue
+            for col, (kre, kim) in cols.items():
+                want = row["ranks"][tab["columns"].index(col)]
+                mode = hb.GRID_CLOSED if tab["dprime"] is None else hb.GRID_INTERIOR
+                r = ctx.rank_complex(hb.make_kernel(kre), hb.make_kernel(kim),
+                                     hb.make_pair(tab["d"], tab["dprime"], row["N"], mode, 0), [1e-12])[0]
+                n_cases += 1
+                if r.rank != want or r.certificate not in (1, 2):
+                    bad.append((tab["label"], row["N"], col, want, r.rank, r.gap, r.certificate))
+    assert n_cases >= 28
+    assert not bad, bad
+
+
+@pytest.mark.parametrize("d,dp,col", [(2, 1, "F3"), (3, 2, "F4"), (2, None, "F4"), (3, 0, "F3")])
+def test_complex_rank_matches_oracle_uniform(ctx, hb, oracle, d, dp, col):
+    kre, kim = oracle.COMPLEX_COLUMNS[col]
+    n, seed = 700, 17
+    r = ctx.rank_complex(hb.make_kernel(kre), hb.make_kernel(kim),
+                         hb.make_pair(d, dp, n, hb.UNIFORM, seed), [1e-12, 1e-8])
+    o = oracle.rank_problem_complex(d, dp, kre, kim, n, [1e-12, 1e-8], seed=seed)
+    assert [x.rank for x in r] == [x.rank for x in o]
+    assert all(x.rank_lo == x.rank_hi for x in r)
+    assert abs(r[0].sigma1 - o[0].sigma1) <= 1e-12 * o[0].sigma1
+
+
 @pytest.mark.slow
 def test_paper_tables_large_n(ctx, hb, paper_tables):
     """Published values at the paper's large N, where no CPU SVD is practical (e.g. 3D face

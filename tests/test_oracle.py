@@ -164,6 +164,28 @@ def test_oracle_reproduces_paper_table(oracle, label, d, dp, n, kname, want):
     assert rec.rank == want, f"{label} N={n} {kname}: {rec.rank} != {want} (gap {rec.gap:.2e})"
 
 
+# the complex columns F3 = e^{ir}/r and F4 = H_2^(1)(r) at each table's first N, for the tables
+# whose first N keeps a CPU complex SVD short (1-D and 3-D; the GPU test covers all 14 tables)
+def _first_rows_complex(tables):
+    for tab in tables:
+        row = tab["rows"][0]
+        if tab["d"] not in (1, 3):
+            continue
+        for col in ("F3", "F4"):
+            yield tab["label"], tab["d"], tab["dprime"], row["N"], col, row["ranks"][tab["columns"].index(col)]
+
+
+@pytest.mark.parametrize("label,d,dp,n,col,want", list(_first_rows_complex(
+    __import__("json").loads((__import__("pathlib").Path(__file__).parent / "golden" /
+                              "paper_tables.json").read_text()))))
+def test_oracle_reproduces_paper_complex_columns(oracle, label, d, dp, n, col, want):
+    kre, kim = oracle.COMPLEX_COLUMNS[col]
+    mode = oracle.GRID_CLOSED if dp is None else oracle.GRID_INTERIOR
+    rec = oracle.rank_problem_complex(d, dp, kre, kim, n, [1e-12], mode=mode, seed=0,
+                                      nthreads=nthreads())[0]
+    assert rec.rank == want, f"{label} N={n} {col}: {rec.rank} != {want} (gap {rec.gap:.2e})"
+
+
 def test_golden_baseline_fixture_consistent(oracle, baseline_ranks):
     """The committed BASELINE-config oracle ranks reproduce (cheap N=1000 entries)."""
     recs = [r for r in baseline_ranks if r["N"] == 1000 and r["d"] <= 2]
