@@ -4,6 +4,9 @@
 //              [--epsilon 1e-12] [--grid uniform|interior|closed] [--seed S] [--devices 0[,1..]]
 //              [--out file.csv]
 //
+// NAME is a catalog kernel (kernel.hpp:112-129) or one of the paper's complex columns
+// "helmholtz3d" (F3 = e^{ir}/r) and "hankel_h12" (F4 = H_2^(1)(r)), ranked as K_re + i·K_im.
+//
 // Prints the CSV of SPEC.md:613 (plus certification columns).  Exit codes (SPEC.md:666,
 // run_rank_bench): 0 success, 2 some problems skipped by a guard (ENOMEM/ECAP), 1 error,
 // 64 usage error (missing / malformed flag).
@@ -53,7 +56,17 @@ int main(int argc, char** argv) {
     const int d = std::stoi(a["d"]);
     const auto inter = hb200::InteractionClass::parse(a["interaction"]);
     std::vector<hb200::KernelSpec> kernels;
-    for (const auto& k : split(a["kernel"])) kernels.push_back(hb200::kernel_from_string(k));
+    std::vector<std::pair<hb200::KernelSpec, hb200::KernelSpec>> complex_kernels;
+    for (const auto& k : split(a["kernel"])) {
+      if (k == "helmholtz3d")  // F3
+        complex_kernels.push_back({hb200::kernel_from_string("helmholtz3d_re"),
+                                   hb200::kernel_from_string("helmholtz3d_im")});
+      else if (k == "hankel_h12")  // F4
+        complex_kernels.push_back({hb200::kernel_from_string("hankel_h12_re"),
+                                   hb200::kernel_from_string("hankel_h12_im")});
+      else
+        kernels.push_back(hb200::kernel_from_string(k));
+    }
     std::vector<int64_t> ns;
     for (const auto& n : split(a["N"])) ns.push_back(std::stoll(n));
     const double eps = a.count("epsilon") ? std::stod(a["epsilon"]) : 1e-12;
@@ -70,7 +83,26 @@ int main(int argc, char** argv) {
       for (const auto& s : split(a["devices"])) devs.push_back(std::stoi(s));
     }
     std::vector<hb_status> st;
-    const auto recs = hb200::rank_table(kernels, inter, d, ns, eps, devs, mode, seed, &st);
+    auto recs = kernels.empty() ? std::vector<hb200::RankRecord>{}
+                                : hb200::rank_table(kernels, inter, d, ns, eps, devs, mode, seed, &st);
+    if (!complex_kernels.empty()) {  // complex columns: one problem at a time on the first device
+      hb200::Device dev(devs.front());
+      for (const auto& kk : complex_kernels)
+        for (const int64_t n : ns) {
+          const uint64_t ps = mode == hb200::PointMode::Uniform ? hb200::problem_seed(seed, d, inter, n) : seed;
+          const auto g = hb200::pair_geometry(d, inter, n, mode, ps);
+          try {
+            recs.push_back(hb200::epsilon_rank_complex(dev, kk.first, kk.second, g, {eps}).front());
+            st.push_back(HB_OK);
+          } catch (const std::length_error&) {
+            hb200::RankRecord r;
+            r.kernel = hb200::kernel_name(kk.first) + "+i*" + hb200::kernel_name(kk.second);
+            r.N = n;
+            recs.push_back(r);
+            st.push_back(HB_ECAP);
+          }
+        }
+    }
     std::ofstream f;
     std::ostream* os = &std::cout;
     if (a.count("out")) {

@@ -28,6 +28,13 @@ def test_cli_usage_errors():
       "--grid", "interior"], 104),  # SPEC.md:637 example (paper 2D vertex F1, N=10000)
     (["--d", "3", "--interaction", "surface:2", "--kernel", "one_over_r", "--N", "1000",
       "--grid", "interior"], 312),
+    # complex columns (PAPER.md:1357-1369 3-D face F3 / F4 at N = 125; :682-692 2-D vertex F4)
+    (["--d", "3", "--interaction", "surface:2", "--kernel", "helmholtz3d", "--N", "125",
+      "--grid", "interior"], 99),
+    (["--d", "3", "--interaction", "surface:2", "--kernel", "hankel_h12", "--N", "125",
+      "--grid", "interior"], 119),
+    (["--d", "2", "--interaction", "surface:0", "--kernel", "hankel_h12", "--N", "1600",
+      "--grid", "interior"], 94),
 ])
 def test_cli_paper_values(args, want):
     r = run(*args)
