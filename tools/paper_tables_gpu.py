@@ -1,7 +1,7 @@
 """Every published rank of the paper's 14 tables (tests/golden/paper_tables.json)
 recomputed on the GPU: real columns F1, F2, F5-F8 by hb_rank, complex F3 / F4 by hb_rank_complex
 (real embedding), ε = 1e-12, interior grid near-field / closed grid far-field.
-Usage: python tools/paper_tables_gpu.py [max_n] > log   (JSON line per value, summary last)"""
+Usage: python tools/paper_tables_gpu.py [max_n [min_n]] > log   (JSON line per value, summary last)"""
 import json
 import sys
 import time
@@ -10,6 +10,7 @@ sys.path.insert(0, ".")
 import paper_2209_05819_b200 as hb  # noqa: E402
 
 max_n = int(sys.argv[1]) if len(sys.argv) > 1 else 40000
+min_n = int(sys.argv[2]) if len(sys.argv) > 2 else 0
 tabs = json.load(open("tests/golden/paper_tables.json"))
 cplx = {"F3": ("helmholtz3d_re", "helmholtz3d_im"), "F4": ("hankel_h12_re", "hankel_h12_im")}
 ok = bad = 0
@@ -17,7 +18,7 @@ mism = []
 with hb.Context(0) as ctx:
     for tab in tabs:
         for row in tab["rows"]:
-            if row["N"] > max_n:
+            if row["N"] > max_n or row["N"] <= min_n:
                 continue
             mode = hb.GRID_CLOSED if tab["dprime"] is None else hb.GRID_INTERIOR
             pair = hb.make_pair(tab["d"], tab["dprime"], row["N"], mode, 0)
@@ -36,4 +37,4 @@ with hb.Context(0) as ctx:
                 if not good:
                     mism.append(rec)
                 print(json.dumps(rec), flush=True)
-print(json.dumps({"summary": {"max_n": max_n, "equal": ok, "different": bad, "mismatches": mism}}))
+print(json.dumps({"summary": {"min_n": min_n, "max_n": max_n, "equal": ok, "different": bad, "mismatches": mism}}))
