@@ -395,15 +395,26 @@ __global__ void __launch_bounds__(kAcaThreads) aca_sweep_kernel(AcaParams p) {
 }
 
 // L(a,k) = u_k(σ_a) / pivot_k, U(k,b) = pivot_k v_k(τ_b)  (aca.hpp:157-160)
-__global__ void aca_build_lu_kernel(const double* __restrict__ Ua, int64_t m,
-                                    const double* __restrict__ Va, int64_t n,
-                                    const int64_t* __restrict__ sig, const int64_t* __restrict__ tau,
-                                    const double* __restrict__ piv, int64_t r, double* L, double* U) {
-  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (idx >= r * r) return;
-  const int64_t a = idx % r, k = idx / r;  // L column k, row a ; U row k, column a
-  L[a + k * r] = __ddiv_rn(Ua[sig[a] + k * m], piv[k]);
-  U[k + a * r] = __dmul_rn(piv[k], Va[tau[a] + k * n]);
+// L(a,k) = u_k(σ_a) / pivot_k, U(k,b) = pivot_k v_k(τ_b)  (aca.hpp:157-160), every block of a
+// batch in one launch (blockIdx.y = block)
+struct LuJob {
+  const double* Ua;
+  const double* Va;
+  const int64_t* sig;
+  const int64_t* tau;
+  const double* piv;
+  int64_t m, n, r;
+  double* L;
+  double* U;
+};
+__global__ void aca_build_lu_kernel(const LuJob* __restrict__ jobs) {
+  const LuJob J = jobs[blockIdx.y];
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < J.r * J.r;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t a = idx % J.r, k = idx / J.r;  // L column k, row a ; U row k, column a
+    J.L[a + k * J.r] = __ddiv_rn(J.Ua[J.sig[a] + k * J.m], J.piv[k]);
+    J.U[k + a * J.r] = __dmul_rn(J.piv[k], J.Va[J.tau[a] + k * J.n]);
+  }
 }
 
 // t_k = K(σ_k, J) · q  (aca.hpp:207); one CTA per k, fixed-order reduction
@@ -475,6 +486,8 @@ struct SweepBufs {
   unsigned char *used_row = nullptr, *used_col = nullptr;
   AcaState* st = nullptr;
   unsigned int* bar = nullptr;
+  bool own_uvp = false;  // U, V, part individually allocated (after growth); the rest lives in
+                         // the per-call arena
 };
 
 template <typename T>
@@ -488,11 +501,23 @@ void dfree(void* p, cudaStream_t s) {
 }
 
 void free_bufs(SweepBufs& b, cudaStream_t s) {
-  for (void* p : {(void*)b.U, (void*)b.V, (void*)b.piv, (void*)b.rowbuf, (void*)b.part, (void*)b.sig,
-                  (void*)b.tau, (void*)b.used_row, (void*)b.used_col, (void*)b.st, (void*)b.bar})
-    dfree(p, s);
+  if (b.own_uvp)
+    for (void* p : {(void*)b.U, (void*)b.V, (void*)b.part}) dfree(p, s);
   b = SweepBufs{};
 }
+
+// One stream-ordered allocation per run_sweeps call, carved by buffer kind so the per-block
+// states / pivots / flags of a whole batch move with one copy or memset each.
+struct Arena {
+  char* base = nullptr;
+  size_t used = 0;
+  template <typename T>
+  T* take(size_t n) {
+    T* p = reinterpret_cast<T*>(base + used);
+    used += round_up((int64_t)(std::max<size_t>(n, 1) * sizeof(T)), 256);
+    return p;
+  }
+};
 
 }  // namespace
 
@@ -506,43 +531,79 @@ struct AcaBlockReq {
   uint32_t bad = 0;
   SweepBufs bufs;
   int64_t lim = 0;
+  std::vector<double> piv_h;  // pivots (host), filled when the sweep finished
+  std::vector<int64_t> sig_h, tau_h;  // block-local pivot ids (host)
 };
 
-// Run the sweeps of `reqs` (all with the same G) to completion, growing U / V on demand.
+// Run the sweeps of `reqs` (all with the same G) to completion, growing U / V on demand.  The
+// buffers of all blocks come from one arena (kept alive in `arenas` until the caller is done).
 static void run_sweeps(hb_context* c, const DevKernel& K, const double* x, int64_t nt, const double* y,
-                       int64_t ns, int d, std::vector<AcaBlockReq*>& reqs, int G) {
+                       int64_t ns, int d, std::vector<AcaBlockReq*>& reqs, int G,
+                       std::vector<void*>& arenas) {
   cudaStream_t st = c->stream;
   const size_t kCapBudget = (size_t)1 << 31;  // initial U+V bytes per block before growth
+  const size_t nb = reqs.size();
+  static const int64_t init_cap = [] {  // test hook: exercise the growth path
+    const char* e = getenv("HB_ACA_INIT_CAP");
+    return e ? std::max<int64_t>(1, atoll(e)) : (int64_t)0;
+  }();
+  int64_t sum_lim = 0, sum_m = 0, sum_n = 0, sum_mcap = 0, sum_ncap = 0, sum_part = 0;
   for (AcaBlockReq* q : reqs) {
     const int64_t m = q->blk.rows, n = q->blk.cols;
     q->lim = std::min({m, n, q->max_rank});
     SweepBufs& b = q->bufs;
+    b = SweepBufs{};
     b.G = G;
     b.cap = std::min<int64_t>(q->lim, std::max<int64_t>(64, (int64_t)(kCapBudget / (8 * (m + n)))));
-    if (const char* e = getenv("HB_ACA_INIT_CAP"))  // test hook: exercise the growth path
-      b.cap = std::min<int64_t>(q->lim, std::max<int64_t>(1, atoll(e)));
-    b.U = dalloc<double>((size_t)(m * b.cap), st);
-    b.V = dalloc<double>((size_t)(n * b.cap), st);
-    b.piv = dalloc<double>((size_t)q->lim, st);
-    b.sig = dalloc<int64_t>((size_t)q->lim, st);
-    b.tau = dalloc<int64_t>((size_t)q->lim, st);
-    b.rowbuf = dalloc<double>((size_t)n, st);
-    b.part = dalloc<double>((size_t)PartLayout::elems(G, b.cap), st);
-    b.used_row = dalloc<unsigned char>((size_t)m, st);
-    b.used_col = dalloc<unsigned char>((size_t)n, st);
-    b.st = dalloc<AcaState>(1, st);
-    b.bar = dalloc<unsigned int>(64, st);
-    HB_CUDA(cudaMemsetAsync(b.used_row, 0, (size_t)m, st));
-    HB_CUDA(cudaMemsetAsync(b.used_col, 0, (size_t)n, st));
-    HB_CUDA(cudaMemsetAsync(b.bar, 0, 64 * sizeof(unsigned int), st));
-    AcaState s0{};
-    s0.rank = 0;
-    s0.next_row = 0;
-    s0.rows_left = m;
-    s0.fro2 = 0.0;
-    HB_CUDA(cudaMemcpyAsync(b.st, &s0, sizeof(s0), cudaMemcpyHostToDevice, st));
-    HB_CUDA(cudaStreamSynchronize(st));  // s0 is a stack object
+    if (init_cap) b.cap = std::min<int64_t>(q->lim, init_cap);
+    sum_lim += round_up(q->lim, 32);
+    sum_m += round_up(m, 256);
+    sum_n += round_up(n, 256);
+    sum_mcap += round_up(m * b.cap, 32);
+    sum_ncap += round_up(n * b.cap, 32);
+    sum_part += round_up(PartLayout::elems(G, b.cap), 32);
   }
+  // layout by kind: [states][bars][used_row][used_col] (zeroed / uploaded together), then
+  // [piv][sig][tau], [rowbuf], [part], [U], [V]
+  const size_t bytes = (nb * sizeof(AcaState) + 256) + (nb * 64 * sizeof(unsigned int) + 256) +
+                       (size_t)(sum_m + sum_n) + 512 + (size_t)sum_lim * 24 + 768 +
+                       (size_t)(sum_n + sum_part + sum_mcap + sum_ncap) * 8 + 1024 + nb * 4 * 256;
+  void* raw = nullptr;
+  HB_CUDA(cudaMallocAsync(&raw, bytes, st));
+  arenas.push_back(raw);
+  Arena ar{static_cast<char*>(raw), 0};
+  AcaState* states = ar.take<AcaState>(nb);
+  unsigned int* bars = ar.take<unsigned int>(nb * 64);
+  unsigned char* urow = ar.take<unsigned char>((size_t)sum_m);
+  unsigned char* ucol = ar.take<unsigned char>((size_t)sum_n);
+  const size_t zero_bytes = (size_t)(reinterpret_cast<char*>(ucol) - reinterpret_cast<char*>(bars)) + (size_t)sum_n;
+  std::vector<AcaState> s0(nb);
+  int64_t om = 0, on = 0;
+  for (size_t i = 0; i < nb; ++i) {
+    AcaBlockReq* q = reqs[i];
+    SweepBufs& b = q->bufs;
+    b.st = states + i;
+    b.bar = bars + 64 * i;
+    b.used_row = urow + om;
+    b.used_col = ucol + on;
+    om += round_up(q->blk.rows, 256);
+    on += round_up(q->blk.cols, 256);
+    s0[i].rank = 0;
+    s0[i].next_row = 0;
+    s0[i].rows_left = q->blk.rows;
+    s0[i].fro2 = 0.0;
+  }
+  for (AcaBlockReq* q : reqs) q->bufs.piv = ar.take<double>((size_t)q->lim);
+  for (AcaBlockReq* q : reqs) q->bufs.sig = ar.take<int64_t>((size_t)q->lim);
+  for (AcaBlockReq* q : reqs) q->bufs.tau = ar.take<int64_t>((size_t)q->lim);
+  for (AcaBlockReq* q : reqs) q->bufs.rowbuf = ar.take<double>((size_t)q->blk.cols);
+  for (AcaBlockReq* q : reqs) q->bufs.part = ar.take<double>((size_t)PartLayout::elems(G, q->bufs.cap));
+  for (AcaBlockReq* q : reqs) q->bufs.U = ar.take<double>((size_t)(q->blk.rows * q->bufs.cap));
+  for (AcaBlockReq* q : reqs) q->bufs.V = ar.take<double>((size_t)(q->blk.cols * q->bufs.cap));
+  HB_REQUIRE(ar.used <= bytes, HB_ECUDA, "aca: arena layout overflow");
+  HB_CUDA(cudaMemsetAsync(bars, 0, zero_bytes, st));
+  // pageable source: the call returns once the data is staged, so s0 may go out of scope
+  HB_CUDA(cudaMemcpyAsync(states, s0.data(), nb * sizeof(AcaState), cudaMemcpyHostToDevice, st));
   std::vector<AcaBlockReq*> live = reqs;
   while (!live.empty()) {
     std::vector<AcaBlockDev> hb(live.size());
@@ -619,8 +680,12 @@ static void run_sweeps(hb_context* c, const DevKernel& K, const double* x, int64
     }
     if (sync_debug_enabled()) debug_sync_after_launch(__FILE__, __LINE__);
     std::vector<AcaState> hs(live.size());
-    for (size_t i = 0; i < live.size(); ++i)
-      HB_CUDA(cudaMemcpyAsync(&hs[i], live[i]->bufs.st, sizeof(AcaState), cudaMemcpyDeviceToHost, st));
+    if (live.size() == nb) {  // first round: all states contiguous, one copy
+      HB_CUDA(cudaMemcpyAsync(hs.data(), states, nb * sizeof(AcaState), cudaMemcpyDeviceToHost, st));
+    } else {
+      for (size_t i = 0; i < live.size(); ++i)
+        HB_CUDA(cudaMemcpyAsync(&hs[i], live[i]->bufs.st, sizeof(AcaState), cudaMemcpyDeviceToHost, st));
+    }
     HB_CUDA(cudaStreamSynchronize(st));
     dfree(dblocks, st);
     std::vector<AcaBlockReq*> next;
@@ -639,17 +704,36 @@ static void run_sweeps(hb_context* c, const DevKernel& K, const double* x, int64
         double* V2 = dalloc<double>((size_t)(n * ncap), st);
         HB_CUDA(cudaMemcpyAsync(U2, b.U, sizeof(double) * m * b.cap, cudaMemcpyDeviceToDevice, st));
         HB_CUDA(cudaMemcpyAsync(V2, b.V, sizeof(double) * n * b.cap, cudaMemcpyDeviceToDevice, st));
-        dfree(b.U, st);
-        dfree(b.V, st);
-        dfree(b.part, st);
+        if (b.own_uvp) {
+          dfree(b.U, st);
+          dfree(b.V, st);
+          dfree(b.part, st);
+        }
         b.U = U2;
         b.V = V2;
         b.cap = ncap;
         b.part = dalloc<double>((size_t)PartLayout::elems(b.G, b.cap), st);
+        b.own_uvp = true;
         next.push_back(q);
       }
     }
     live.swap(next);
+  }
+  // pivots and pivot ids of the whole batch: the [piv][sig][tau] pieces are contiguous in the
+  // arena, so one copy brings them all to the host
+  const char* lo = reinterpret_cast<const char*>(reqs.front()->bufs.piv);
+  const char* hi = reinterpret_cast<const char*>(reqs.back()->bufs.tau + std::max<int64_t>(reqs.back()->lim, 1));
+  std::vector<char> h((size_t)(hi - lo));
+  HB_CUDA(cudaMemcpyAsync(h.data(), lo, h.size(), cudaMemcpyDeviceToHost, st));
+  HB_CUDA(cudaStreamSynchronize(st));
+  for (AcaBlockReq* q : reqs) {
+    const size_t r = (size_t)q->rank;
+    const double* pv = reinterpret_cast<const double*>(h.data() + (reinterpret_cast<const char*>(q->bufs.piv) - lo));
+    const int64_t* sg = reinterpret_cast<const int64_t*>(h.data() + (reinterpret_cast<const char*>(q->bufs.sig) - lo));
+    const int64_t* tu = reinterpret_cast<const int64_t*>(h.data() + (reinterpret_cast<const char*>(q->bufs.tau) - lo));
+    q->piv_h.assign(pv, pv + r);
+    q->sig_h.assign(sg, sg + r);
+    q->tau_h.assign(tu, tu + r);
   }
 }
 
@@ -693,6 +777,12 @@ void aca_compress(hb_context* c, const hb_kernel& kern, const double* x, int64_t
     reqs[(size_t)i].eps = eps;
     reqs[(size_t)i].max_rank = max_rank;
   }
+  std::vector<void*> arenas;
+  auto release = [&]() {
+    for (auto& r : reqs) free_bufs(r.bufs, st);
+    for (void* p : arenas) dfree(p, st);
+    arenas.clear();
+  };
   auto run_all = [&](std::vector<AcaBlockReq*>& v) {
     std::vector<AcaBlockReq*> small;
     for (AcaBlockReq* q : v) {
@@ -701,69 +791,93 @@ void aca_compress(hb_context* c, const hb_kernel& kern, const double* x, int64_t
         small.push_back(q);
       } else {
         std::vector<AcaBlockReq*> one{q};
-        run_sweeps(c, K, x, nt, y, ns, d, one, G);
+        run_sweeps(c, K, x, nt, y, ns, d, one, G, arenas);
       }
     }
-    if (!small.empty()) run_sweeps(c, K, x, nt, y, ns, d, small, 1);
+    if (!small.empty()) run_sweeps(c, K, x, nt, y, ns, d, small, 1, arenas);
   };
-  std::vector<AcaBlockReq*> all;
-  for (auto& q : reqs) all.push_back(&q);
-  run_all(all);
-  // degenerate pivots: one more sweep at eps/10 (aca.hpp:184)
-  std::vector<std::vector<double>> piv((size_t)nb);
-  auto read_piv = [&](AcaBlockReq& q, std::vector<double>& pv) {
-    pv.assign((size_t)q.rank, 0.0);
-    if (q.rank)
-      HB_CUDA(cudaMemcpyAsync(pv.data(), q.bufs.piv, sizeof(double) * q.rank, cudaMemcpyDeviceToHost, st));
-  };
-  for (int64_t i = 0; i < nb; ++i) read_piv(reqs[(size_t)i], piv[(size_t)i]);
-  HB_CUDA(cudaStreamSynchronize(st));
-  std::vector<AcaBlockReq*> redo;
-  for (int64_t i = 0; i < nb; ++i) {
-    AcaBlockReq& q = reqs[(size_t)i];
-    if (q.bad) {
-      for (auto& r : reqs) free_bufs(r.bufs, st);
-      throw Error(HB_ESINGULAR, "kernel eval: r == 0 on a singular kernel with no diagonal value");
+  try {
+    std::vector<AcaBlockReq*> all;
+    for (auto& q : reqs) all.push_back(&q);
+    run_all(all);
+    // degenerate pivots: one more sweep at eps/10 (aca.hpp:184)
+    std::vector<AcaBlockReq*> redo;
+    for (auto& q : reqs) {
+      if (q.bad) throw Error(HB_ESINGULAR, "kernel eval: r == 0 on a singular kernel with no diagonal value");
+      int64_t keep = 0;
+      if (degenerate_piv(q.piv_h, q.rank, &keep)) {
+        free_bufs(q.bufs, st);
+        q.eps = eps / 10.0;
+        redo.push_back(&q);
+      }
     }
-    int64_t keep = 0;
-    if (degenerate_piv(piv[(size_t)i], q.rank, &keep)) {
-      free_bufs(q.bufs, st);
-      q.eps = eps / 10.0;
-      redo.push_back(&q);
+    if (!redo.empty()) run_all(redo);
+    // factors: L / U of every block from one allocation, built by one launch
+    std::vector<int64_t> rk((size_t)nb);
+    int64_t tot = 0;
+    for (int64_t i = 0; i < nb; ++i) {
+      AcaBlockReq& q = reqs[(size_t)i];
+      int64_t r = q.rank, keep = r;
+      if (degenerate_piv(q.piv_h, r, &keep)) r = keep;  // aca.hpp:185-196
+      rk[(size_t)i] = r;
+      tot += 2 * r * r;
     }
-  }
-  if (!redo.empty()) {
-    run_all(redo);
-    for (AcaBlockReq* q : redo) read_piv(*q, piv[(size_t)(q - reqs.data())]);
+    std::shared_ptr<double> store;
+    if (tot > 0) {
+      double* p = nullptr;
+      HB_CUDA(cudaMalloc(&p, sizeof(double) * (size_t)tot));
+      const int dev = c->device;
+      store = std::shared_ptr<double>(p, [dev](double* q) {
+        cudaSetDevice(dev);
+        cudaFree(q);
+      });
+    }
+    std::vector<LuJob> jobs;
+    int64_t off = 0, rmax = 0;
+    for (int64_t i = 0; i < nb; ++i) {
+      AcaBlockReq& q = reqs[(size_t)i];
+      const int64_t r = rk[(size_t)i];
+      auto* f = new hb_aca_factor();
+      out[i] = f;
+      f->device = c->device;
+      f->rank = (int32_t)r;
+      f->met = q.met;
+      f->sigma.assign(q.sig_h.begin(), q.sig_h.begin() + r);
+      f->tau.assign(q.tau_h.begin(), q.tau_h.begin() + r);
+      for (int64_t k = 0; k < r; ++k) {
+        f->sigma[(size_t)k] += q.blk.row_begin;
+        f->tau[(size_t)k] += q.blk.col_begin;
+      }
+      if (r > 0) {
+        f->store = store;
+        f->L = store.get() + off;
+        f->U = f->L + r * r;
+        off += 2 * r * r;
+        jobs.push_back(LuJob{q.bufs.U, q.bufs.V, q.bufs.sig, q.bufs.tau, q.bufs.piv, q.blk.rows, q.blk.cols, r,
+                             f->L, f->U});
+        rmax = std::max(rmax, r);
+      }
+    }
+    if (!jobs.empty()) {
+      LuJob* dj = dalloc<LuJob>(jobs.size(), st);
+      HB_CUDA(cudaMemcpyAsync(dj, jobs.data(), jobs.size() * sizeof(LuJob), cudaMemcpyHostToDevice, st));
+      for (size_t j0 = 0; j0 < jobs.size(); j0 += 65535) {
+        const unsigned ny = (unsigned)std::min<size_t>(65535, jobs.size() - j0);
+        const unsigned nx = (unsigned)std::min<int64_t>(1024, ceil_div(rmax * rmax, 256));
+        aca_build_lu_kernel<<<dim3(nx, ny), 256, 0, st>>>(dj + j0);
+        HB_LAUNCH_CHECK();
+      }
+      dfree(dj, st);
+    }
+    release();
     HB_CUDA(cudaStreamSynchronize(st));
-  }
-  for (int64_t i = 0; i < nb; ++i) {
-    AcaBlockReq& q = reqs[(size_t)i];
-    int64_t r = q.rank;
-    int64_t keep = r;
-    if (degenerate_piv(piv[(size_t)i], r, &keep)) r = keep;  // aca.hpp:185-196
-    auto* f = new hb_aca_factor();
-    f->device = c->device;
-    f->rank = (int32_t)r;
-    f->met = q.met;
-    f->sigma.assign((size_t)r, 0);
-    f->tau.assign((size_t)r, 0);
-    if (r > 0) {
-      HB_CUDA(cudaMemcpyAsync(f->sigma.data(), q.bufs.sig, sizeof(int64_t) * r, cudaMemcpyDeviceToHost, st));
-      HB_CUDA(cudaMemcpyAsync(f->tau.data(), q.bufs.tau, sizeof(int64_t) * r, cudaMemcpyDeviceToHost, st));
-      HB_CUDA(cudaMalloc(&f->L, sizeof(double) * r * r));
-      HB_CUDA(cudaMalloc(&f->U, sizeof(double) * r * r));
-      aca_build_lu_kernel<<<(unsigned)ceil_div(r * r, 256), 256, 0, st>>>(
-          q.bufs.U, q.blk.rows, q.bufs.V, q.blk.cols, q.bufs.sig, q.bufs.tau, q.bufs.piv, r, f->L, f->U);
-      HB_LAUNCH_CHECK();
+  } catch (...) {
+    for (int64_t i = 0; i < nb; ++i) {
+      delete out[i];
+      out[i] = nullptr;
     }
-    free_bufs(q.bufs, st);
-    HB_CUDA(cudaStreamSynchronize(st));
-    for (int64_t k = 0; k < r; ++k) {
-      f->sigma[(size_t)k] += q.blk.row_begin;
-      f->tau[(size_t)k] += q.blk.col_begin;
-    }
-    out[i] = f;
+    release();
+    throw;
   }
 }
 

@@ -1,6 +1,7 @@
 // hb_context: per-device, per-host-thread state (stream, workspace, barrier slot).
 #pragma once
 
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -49,10 +50,7 @@ struct hb_aca_factor {
   std::vector<int64_t> sigma, tau;  // global target / source ids
   double* L = nullptr;              // device, rank x rank column-major (unit lower)
   double* U = nullptr;              // device, rank x rank column-major (upper)
-  ~hb_aca_factor() {
-    if (L) cudaFree(L);
-    if (U) cudaFree(U);
-  }
+  std::shared_ptr<double> store;    // the batch's L / U allocation (shared by its factors)
 };
 
 namespace hb {
