@@ -58,7 +58,7 @@ namespace hb {
 enum BufId {
   B_A, B_X, B_Y, B_OMEGA, B_YSK, B_YS, B_NRM, B_V, B_W, B_W2, B_S, B_T, B_Z, B_TAU, B_SLOTS,
   B_PIV, B_SWAPS, B_RDIAG, B_EST, B_BEFF, B_PERM, B_FRO, B_FROSUM, B_SPLITK, B_CERT_B, B_CERT_M,
-  B_D, B_E, B_BW, B_BV, B_SCAL, B_FLAGS, B_QUERY, B_ANSWER, B_SIG1, B_CERT_B2, B_PROG, B_ST1_P, B_ST1_X, B_ST1_X2, B_ST1_VT, B_PSCAL, B_TSUB, B_PX, B_PY, B_PN, B_SKCAND, B_TG, B_COUNT
+  B_D, B_E, B_BW, B_BV, B_SCAL, B_FLAGS, B_QUERY, B_ANSWER, B_SIG1, B_CERT_B2, B_PROG, B_ST1_P, B_ST1_X, B_ST1_X2, B_ST1_VT, B_PSCAL, B_TSUB, B_PX, B_PY, B_PN, B_SKCAND, B_TG, B_RDIAG2, B_COUNT
 };
 
 template <typename T>
