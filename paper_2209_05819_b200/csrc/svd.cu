@@ -501,21 +501,12 @@ __global__ void __launch_bounds__(256) bulge_chase_kernel(double* __restrict__ B
         __threadfence();
       }
       const int len = (int)(tk.hi - tk.lo + 1);
-      // reflector from the segment (warp 0, two elements per lane)
-      if (warp == 0) {
-        double x[2];
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int el = lane + 32 * h;
-          x[h] = 0.0;
-          if (el < len) {
-            const int64_t r = tk.right ? tk.idx : tk.lo + el;
-            const int64_t c = tk.right ? tk.lo + el : tk.idx;
-            x[h] = __ldcg(Bd + band_off(r, c, nb, W));
-          }
-        }
-        const double alpha = __shfl_sync(0xffffffffu, x[0], 0);
-        double ss = (lane > 0 ? x[0] * x[0] : 0.0) + x[1] * x[1];
+      // The reflector's segment is the first row (R task: row idx = alo) / first column (L task:
+      // column idx = alo) of the block the task updates, so one L2 round trip loads both: the
+      // block goes to registers, the segment is taken from them (R) or staged in shared memory (L).
+      auto reflector = [&](double x0, double x1) {  // warp 0: x0 / x1 = elements lane / lane + 32
+        const double alpha = __shfl_sync(0xffffffffu, x0, 0);
+        double ss = (lane > 0 ? x0 * x0 : 0.0) + x1 * x1;
         ss = warp_sum(ss);
         double tau = 0.0, scal = 0.0, beta = alpha;
         if (ss > 0.0) {
@@ -523,28 +514,29 @@ __global__ void __launch_bounds__(256) bulge_chase_kernel(double* __restrict__ B
           tau = (beta - alpha) / beta;
           scal = 1.0 / (alpha - beta);
         }
-        v[lane] = lane == 0 ? 1.0 : (lane < len ? x[0] * scal : 0.0);
-        v[lane + 32] = lane + 32 < len ? x[1] * scal : 0.0;
+        v[lane] = lane == 0 ? 1.0 : (lane < len ? x0 * scal : 0.0);
+        v[lane + 32] = lane + 32 < len ? x1 * scal : 0.0;
         if (lane == 0) { sh[0] = tau; sh[1] = beta; }
-      }
-      __syncthreads();
-      const double tau = sh[0];
-      if (tau != 0.0) {
-        if (tk.right) {
-          // rows r in [alo, ahi] (<= 127): s_r = sum_c M[r, lo + c] v_c; M[r, .] -= tau s_r v.
-          // A warp owns up to 16 rows; all loads are issued before the reductions.
-          constexpr int RMAX = 16;
-          const double v0 = v[lane], v1 = v[lane + 32];
-          double m0[RMAX], m1[RMAX], sr[RMAX];
+      };
+      if (tk.right) {
+        // rows r in [alo, ahi] (<= 127): s_r = sum_c M[r, lo + c] v_c; M[r, .] -= tau s_r v.
+        // A warp owns up to 16 rows; all loads are issued before the reductions.
+        constexpr int RMAX = 16;
+        double m0[RMAX], m1[RMAX], sr[RMAX];
 #pragma unroll
-          for (int j = 0; j < RMAX; ++j) {
-            const int64_t r = tk.alo + warp + (int64_t)j * NW;
-            const int64_t c0 = tk.lo + lane, c1 = c0 + 32;
-            const bool ok0 = r <= tk.ahi && lane < len && band_in(r, c0, nb);
-            const bool ok1 = r <= tk.ahi && lane + 32 < len && band_in(r, c1, nb);
-            m0[j] = ok0 ? __ldcg(Bd + band_off(r, c0, nb, W)) : 0.0;
-            m1[j] = ok1 ? __ldcg(Bd + band_off(r, c1, nb, W)) : 0.0;
-          }
+        for (int j = 0; j < RMAX; ++j) {
+          const int64_t r = tk.alo + warp + (int64_t)j * NW;
+          const int64_t c0 = tk.lo + lane, c1 = c0 + 32;
+          const bool ok0 = r <= tk.ahi && lane < len && band_in(r, c0, nb);
+          const bool ok1 = r <= tk.ahi && lane + 32 < len && band_in(r, c1, nb);
+          m0[j] = ok0 ? __ldcg(Bd + band_off(r, c0, nb, W)) : 0.0;
+          m1[j] = ok1 ? __ldcg(Bd + band_off(r, c1, nb, W)) : 0.0;
+        }
+        if (warp == 0) reflector(m0[0], m1[0]);  // row alo == idx: the segment
+        __syncthreads();
+        const double tau = sh[0];
+        if (tau != 0.0) {
+          const double v0 = v[lane], v1 = v[lane + 32];
 #pragma unroll
           for (int j = 0; j < RMAX; ++j) sr[j] = m0[j] * v0 + m1[j] * v1;
 #pragma unroll
@@ -560,25 +552,38 @@ __global__ void __launch_bounds__(256) bulge_chase_kernel(double* __restrict__ B
             if (r <= tk.ahi && lane + 32 < len && band_in(r, c1, nb))
               __stcg(Bd + band_off(r, c1, nb, W), m1[j] - tau * sr[j] * v1);
           }
-        } else {
-          // columns c in [alo, ahi] (<= 128): thread (cc, half) holds 32 rows of column cc;
-          // w_c = sum_r v_r M[lo + r, c] combined over the two halves; M[., c] -= tau v w_c.
-          const int ncols = (int)(tk.ahi - tk.alo + 1);
-          const int cc = tid & 127, half = tid >> 7;
-          const int64_t c = tk.alo + cc;
-          double x[32];
+        }
+      } else {
+        // columns c in [alo, ahi] (<= 128): thread (cc, half) holds 32 rows of column cc;
+        // w_c = sum_r v_r M[lo + r, c] combined over the two halves; M[., c] -= tau v w_c.
+        const int ncols = (int)(tk.ahi - tk.alo + 1);
+        const int cc = tid & 127, half = tid >> 7;
+        const int64_t c = tk.alo + cc;
+        double x[32];
+        if (cc < ncols) {
+#pragma unroll
+          for (int r = 0; r < 32; ++r) {
+            const int rr = half * 32 + r;
+            const bool ok = rr < len && band_in(tk.lo + rr, c, nb);
+            x[r] = ok ? __ldcg(Bd + band_off(tk.lo + rr, c, nb, W)) : 0.0;
+          }
+        }
+        if (cc == 0) {  // column alo == idx: the segment
+#pragma unroll
+          for (int r = 0; r < 32; ++r) wpart[0][half * 32 + r] = x[r];
+        }
+        __syncthreads();
+        if (warp == 0) reflector(wpart[0][lane], wpart[0][lane + 32]);
+        __syncthreads();
+        const double tau = sh[0];
+        if (tau != 0.0) {
           double w = 0.0;
           if (cc < ncols) {
 #pragma unroll
-            for (int r = 0; r < 32; ++r) {
-              const int rr = half * 32 + r;
-              const bool ok = rr < len && band_in(tk.lo + rr, c, nb);
-              x[r] = ok ? __ldcg(Bd + band_off(tk.lo + rr, c, nb, W)) : 0.0;
-            }
-#pragma unroll
             for (int r = 0; r < 32; ++r) w += v[half * 32 + r] * x[r];
-            wpart[half][cc] = w;
           }
+          __syncthreads();  // wpart[0] held the segment
+          if (cc < ncols) wpart[half][cc] = w;
           __syncthreads();
           if (cc < ncols) {
             w = (wpart[0][cc] + wpart[1][cc]) * tau;
