@@ -487,18 +487,19 @@ __global__ void __launch_bounds__(256) bulge_chase_kernel(double* __restrict__ B
   __shared__ double v[64];
   __shared__ double wpart[2][128];
   __shared__ double sh[4];
-  volatile int* vprog = prog;
   for (int64_t s = blockIdx.x; s < k - 1; s += G) {
     const int prev_n = s > 0 ? chase_ntasks(s - 1, k, nb) : 0;
     ChaseTask tk;
     int t = 0;
     for (; chase_task(s, t, k, nb, &tk); ++t) {
       if (s > 0) {
+        // thread 0 acquires the previous sweep's progress; the CTA barrier then orders every
+        // thread's (L2, __ldcg) loads after it — no per-thread fence (a MEMBAR.SC.GPU in all 256
+        // threads was 84 % of the kernel's stall samples)
         const int need = min(t + 4, prev_n);
         if (tid == 0)
-          while (vprog[s - 1] < need) __nanosleep(32);
+          while ((int)ld_acquire_gpu(reinterpret_cast<const unsigned int*>(prog + s - 1)) < need) __nanosleep(32);
         __syncthreads();
-        __threadfence();
       }
       const int len = (int)(tk.hi - tk.lo + 1);
       // The reflector's segment is the first row (R task: row idx = alo) / first column (L task:
@@ -609,16 +610,11 @@ __global__ void __launch_bounds__(256) bulge_chase_kernel(double* __restrict__ B
           }
         }
       }
-      __syncthreads();
-      if (tid == 0) {
-        __threadfence();
-        atomicExch(prog + s, t + 1);
-      }
+      __syncthreads();  // every thread's (L2, __stcg) stores of this task precede the release
+      if (tid == 0) st_release_gpu(reinterpret_cast<unsigned int*>(prog + s), (unsigned int)(t + 1));
     }
-    if (tid == 0) {
-      __threadfence();
-      atomicExch(prog + s, t + 1000000);  // sweep finished (>= any need)
-    }
+    if (tid == 0)  // sweep finished (>= any need)
+      st_release_gpu(reinterpret_cast<unsigned int*>(prog + s), (unsigned int)(t + 1000000));
   }
 }
 
