@@ -449,6 +449,7 @@ void rank_matrix_inplace(hb_context* c, double* A, int64_t m, int64_t n, int64_t
   SigmaAnswer ans[2 * HB_MAX_TOLS];
   int64_t k = 0;
   int rounds = 0;
+  double last_slope = 0.0;  // log-decay of |R_jj| per index near the threshold (0: unknown)
   for (;; ++rounds) {
     while (j < kmax) {
       const int b_req = (int)std::min<int64_t>({(int64_t)b, kmax - j, (int64_t)kBlockMax});
@@ -595,11 +596,13 @@ void rank_matrix_inplace(hb_context* c, double* A, int64_t m, int64_t n, int64_t
       delta = 0.0;
       delta2 = INFINITY;
     }
-    // Skip a certification that would almost surely leave the bracket open: the window
+    // Skip a certification that would likely leave the bracket open: the window
     // (sqrt(thr² − δ²), thr] has log-width ~η²/2, and where the spectrum is dense near thr
     // (slowly decaying 4-D spectra: ~470 σ per unit of log σ) it holds ~0.6 σ on average at
     // η = 0.05.  The local density comes from the R diagonal (|R_jj| tracks σ_j's decay for a
-    // pivoted QR); a wrong guess costs time only — the certification below stays rigorous.
+    // pivoted QR); when more than 0.1 σ are expected, η drops to the value that expects 0.1
+    // (>= η/5) before the first certification.  A wrong guess costs time only — the
+    // certification below stays rigorous.
     if (j < kmax && rounds < 3 && delta2 == INFINITY && sigma1_est > 0.0) {
       static const bool predict = [] {
         const char* e = getenv("HB_PREDICT_OPEN");
@@ -624,9 +627,15 @@ void rank_matrix_inplace(hb_context* c, double* A, int64_t m, int64_t n, int64_t
           static const bool dbg = getenv("HB_DEBUG_STOP") != nullptr;
           if (dbg) fprintf(stderr, "[predict] j=%lld p~%lld slope=%.3g expected=%.3g eta=%.3g\n", (long long)j,
                            (long long)ph, slope, expected, eta_cur);
-          if (expected > 0.35) {
-            eta_cur *= 0.2;
-            continue;  // next round: factor on to the smaller eta, certify once there
+          last_slope = slope;
+          if (expected > 0.1) {
+            // the η at which ~0.1 σ are expected in the window (never below η/5): factor on to
+            // it and certify once there
+            const double eta_new = std::max(0.2 * eta_cur, std::sqrt(2.0 * 0.1 * slope));
+            if (eta_new < 0.9 * eta_cur) {
+              eta_cur = eta_new;
+              continue;
+            }
           }
         }
       }
@@ -689,7 +698,10 @@ void rank_matrix_inplace(hb_context* c, double* A, int64_t m, int64_t n, int64_t
       open |= cert_kind[t] == 0;
     }
     if (!open || j >= kmax || rounds >= 3) break;
-    eta_cur *= 0.2;
+    // open bracket: with a density estimate, the η expecting ~0.02 σ in the window (in [η/5, η/2]);
+    // without one, η/5
+    eta_cur = last_slope > 0.0 ? std::min(0.5 * eta_cur, std::max(0.2 * eta_cur, std::sqrt(2.0 * 0.02 * last_slope)))
+                               : 0.2 * eta_cur;
   }
   HB_CUDA(cudaEventRecord(c->ev[3], st));
   HB_CUDA(cudaEventSynchronize(c->ev[3]));
