@@ -245,3 +245,32 @@ def test_profiling_stats(ctx, hb):
     assert s["problems"] >= 1 and s["gemm_launches"] > 0 and s["gemm_flops"] > 0
     assert s["phase_ms"]["update"] > 0 and s["phase_ms"]["bidiag"] > 0
     assert s["launches"] > 0
+
+
+@pytest.mark.parametrize("d,dp,kname,nt,ns", [(2, 1, "log_r", 1500, 600), (3, 2, "one_over_r", 400, 1300),
+                                              (4, 3, "exp_neg_r", 900, 1100), (1, 0, "log_r", 3000, 7),
+                                              (2, None, "one_over_r", 5, 2000)])
+def test_rectangular_pairs_match_oracle(ctx, hb, oracle, d, dp, kname, nt, ns):
+    """Ragged blocks (T != N targets / sources, incl. a handful of rows or columns): the ε-rank
+    of the T x N block equals the oracle's LAPACK count."""
+    seed = 4242
+    r = ctx.rank(hb.make_kernel(kname), hb.make_pair(d, dp, nt, hb.UNIFORM, seed, n_source=ns),
+                 [1e-12, 1e-8])
+    x = oracle.points(d, [0.0] * d, 1.0, nt, oracle.UNIFORM, seed, 0)
+    y = oracle.points(d, hb.offset(d, dp), 1.0, ns, oracle.UNIFORM, seed, 1)
+    s = oracle.singular_values(oracle.assemble(oracle.KERNEL_IDS[kname], x, y, nthreads=8))
+    assert [q.rank for q in r] == [oracle.epsilon_rank_from_sigma(s, t).rank for t in (1e-12, 1e-8)]
+    assert all(q.rank_lo == q.rank_hi for q in r)
+
+
+def test_rectangular_complex_pair(ctx, hb, oracle):
+    """hb_rank_complex on a T != N block (the real embedding is 2T x 2N)."""
+    seed, nt, ns = 77, 700, 450
+    r = ctx.rank_complex(hb.make_kernel("helmholtz3d_re"), hb.make_kernel("helmholtz3d_im"),
+                         hb.make_pair(3, 1, nt, hb.UNIFORM, seed, n_source=ns), [1e-12])[0]
+    x = oracle.points(3, [0.0] * 3, 1.0, nt, oracle.UNIFORM, seed, 0)
+    y = oracle.points(3, hb.offset(3, 1), 1.0, ns, oracle.UNIFORM, seed, 1)
+    A = oracle.assemble(oracle.KERNEL_IDS["helmholtz3d_re"], x, y)
+    B = oracle.assemble(oracle.KERNEL_IDS["helmholtz3d_im"], x, y)
+    s = oracle.singular_values(A + 1j * B)
+    assert r.rank == oracle.epsilon_rank_from_sigma(s, 1e-12).rank and r.rank_lo == r.rank_hi
