@@ -126,10 +126,13 @@ class ClockSampler:
         self.lines: list[str] = []
 
     def start(self):
+        if os.environ.get("HB_BENCH_SMI_MS") == "0":  # experiments: no sampler
+            return
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms",
+                 os.environ.get("HB_BENCH_SMI_MS", "100")],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()

@@ -135,8 +135,9 @@ void rank_pair(hb_context* c, const hb_kernel* kernel, const hb_pair* pair, cons
   const int d = pair->target.d;
   const int64_t m = pair->n_target, n = pair->n_source;
   const int64_t lda = hb::round_up(m, 8);
-  size_t free_b = 0, total_b = 0;
-  HB_CUDA(cudaMemGetInfo(&free_b, &total_b));
+  // total device memory cached at context creation: the driver query was seen blocking every
+  // sweep thread for tens of ms at once
+  const size_t total_b = c->total_mem;
   if ((double)lda * n * 8.0 * 1.25 > (double)total_b)
     throw Error(HB_ENOMEM, "K does not fit in device memory");
   HB_CUDA(cudaEventRecord(c->ev[0], c->stream));
@@ -175,8 +176,7 @@ void rank_pair_complex(hb_context* c, const hb_kernel* kre, const hb_kernel* kim
   const int64_t m = pair->n_target, n = pair->n_source;
   const int64_t m2 = 2 * m, n2 = 2 * n;
   const int64_t lda = hb::round_up(m2, 8);
-  size_t free_b = 0, total_b = 0;
-  HB_CUDA(cudaMemGetInfo(&free_b, &total_b));
+  const size_t total_b = c->total_mem;
   if ((double)lda * n2 * 8.0 * 1.25 > (double)total_b)
     throw Error(HB_ENOMEM, "the real embedding does not fit in device memory");
   HB_CUDA(cudaEventRecord(c->ev[0], c->stream));
@@ -606,6 +606,8 @@ hb_status hb_sweep_ex(const hb_problem* probs, int64_t n, const int32_t* devices
       for (int s = 0; s < nsub; ++s) first_q[s] = take(s >= nsub - nback);
       std::vector<std::thread> sth;
       std::mutex sub_mu;
+      std::vector<std::string> trace_lines;
+      const double sweep_t0 = hb::host_now();
       auto sub_worker = [&](int s) {
         hb_status ss = HB_OK;
         hb_context* sc = cached_context(devices[w], 1000 + slot[w] * 16 + s, &ss);
@@ -646,7 +648,26 @@ hb_status hb_sweep_ex(const hb_problem* probs, int64_t n, const int32_t* devices
             cudaEventCreate(&e1);
             cudaEventRecord(e0, sc->stream);
           }
+          const bool ht = hb::host_trace_enabled();
+          const hb::HostTrace h0 = hb::host_trace();
+          const double t0 = ht ? hb::host_now() : 0.0;
           st[small[q]] = hb_rank(sc, &p.kernel, &p.pair, p.tols, p.ntol, out + offset[small[q]]);
+          if (ht) {
+            const hb::HostTrace& h1 = hb::host_trace();
+            char buf[256];
+            snprintf(buf, sizeof buf,
+                     "[hosttrace] stream %d N=%lld d'=%d start %.2f wall %.2f sync %.2f (n %ld max %.2f) "
+                     "coop %.2f (max %.2f) call %.2f @%s gap %.2f @%s ms\n",
+                     s, (long long)p.pair.n_target, p.pair.d_prime, (t0 - sweep_t0) * 1e3,
+                     (hb::host_now() - t0) * 1e3, (h1.sync_s - h0.sync_s) * 1e3, h1.n_sync - h0.n_sync,
+                     h1.max_sync_s * 1e3, (h1.launch_s - h0.launch_s) * 1e3, h1.max_launch_s * 1e3,
+                     h1.max_call_s * 1e3, h1.max_call_at, h1.max_gap_s * 1e3, h1.max_gap_at);
+            hb::host_trace().max_call_s = hb::host_trace().max_gap_s = 0.0;
+            hb::host_trace().max_sync_s = 0.0;
+            hb::host_trace().max_launch_s = 0.0;
+            std::lock_guard<std::mutex> lk(sub_mu);
+            trace_lines.push_back(buf);
+          }
           if (timeline) {  // HB_TIMELINE=1: per-problem device span on its sub-stream (stderr)
             cudaEventRecord(e1, sc->stream);
             cudaEventSynchronize(e1);
@@ -663,6 +684,7 @@ hb_status hb_sweep_ex(const hb_problem* probs, int64_t n, const int32_t* devices
       };
       for (int s = 0; s < nsub; ++s) sth.emplace_back(sub_worker, s);
       for (auto& t : sth) t.join();
+      for (auto& l : trace_lines) fputs(l.c_str(), stderr);
       for (auto* sc : subs) cudaStreamWaitEvent(c->stream, sc->ev[5], 0);
       cudaEventDestroy(ready);
     }

@@ -7,6 +7,7 @@
 #include <atomic>
 #include <cstdio>
 #include <cstdlib>
+#include <chrono>
 #include <map>
 #include <mutex>
 #include <stdexcept>
@@ -16,15 +17,70 @@
 
 namespace hb {
 
+// HB_HOSTTRACE=1 (diagnostics): per host thread, time blocked in stream syncs and in launch calls
+struct HostTrace {
+  double sync_s = 0.0, max_sync_s = 0.0, launch_s = 0.0, max_launch_s = 0.0;
+  long n_sync = 0;
+  double max_call_s = 0.0, max_gap_s = 0.0, last_end = 0.0;
+  const char* max_call_at = "";
+  const char* max_gap_at = "";
+};
+inline HostTrace& host_trace() {
+  thread_local HostTrace t;
+  return t;
+}
+inline bool host_trace_enabled() {
+  static const bool on = getenv("HB_HOSTTRACE") != nullptr;
+  return on;
+}
+inline double host_now() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+// every HB_CUDA call: the longest call and the longest host gap before a call (label = call site)
+inline void host_trace_call(double t0, const char* at) {
+  HostTrace& h = host_trace();
+  const double t1 = host_now();
+  if (t1 - t0 > h.max_call_s) {
+    h.max_call_s = t1 - t0;
+    h.max_call_at = at;
+  }
+  if (h.last_end > 0.0 && t0 - h.last_end > h.max_gap_s) {
+    h.max_gap_s = t0 - h.last_end;
+    h.max_gap_at = at;
+  }
+  h.last_end = t1;
+}
+struct TraceSync {  // scope guard: time inside counts as a host wait for the device
+  double t0;
+  bool launch;
+  explicit TraceSync(bool is_launch = false) : t0(host_trace_enabled() ? host_now() : 0.0), launch(is_launch) {}
+  ~TraceSync() {
+    if (!host_trace_enabled()) return;
+    const double d = host_now() - t0;
+    HostTrace& h = host_trace();
+    if (launch) {
+      h.launch_s += d;
+      h.max_launch_s = std::max(h.max_launch_s, d);
+    } else {
+      h.sync_s += d;
+      h.max_sync_s = std::max(h.max_sync_s, d);
+      h.n_sync++;
+    }
+  }
+};
 // Error carrying an hb_status; converted to a status code at the C ABI (abi.cpp).
 struct Error : std::runtime_error {
   hb_status status;
   Error(hb_status s, const std::string& what) : std::runtime_error(what), status(s) {}
 };
 
+#define HB_STR2(x) #x
+#define HB_STR(x) HB_STR2(x)
 #define HB_CUDA(x)                                                                           \
   do {                                                                                       \
+    const double ht0_ = ::hb::host_trace_enabled() ? ::hb::host_now() : 0.0;                  \
     cudaError_t e_ = (x);                                                                    \
+    if (ht0_ != 0.0) ::hb::host_trace_call(ht0_, __FILE__ ":" HB_STR(__LINE__));             \
     if (e_ != cudaSuccess)                                                                   \
       throw ::hb::Error(e_ == cudaErrorMemoryAllocation ? HB_ENOMEM : HB_ECUDA,              \
                         std::string(#x) + ": " + cudaGetErrorString(e_) + " @" __FILE__ ":" + \

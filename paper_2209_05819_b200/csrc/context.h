@@ -13,6 +13,7 @@ struct hb_context {
   int device = 0;
   cudaStream_t stream = nullptr;
   int num_sms = 148;
+  size_t total_mem = 0;  // bytes of device memory (queried once at creation)
   int coop_sms = 148;  // SM share for cooperative grids (< num_sms when streams run concurrently)
   int priority = 0;    // CUDA stream priority of `stream` (0 = default)
   int block_max = hb::kBlockMax;

@@ -23,7 +23,10 @@ template <typename P>
 void coop(void (*kern)(P), int grid, size_t smem, cudaStream_t st, P prm, int threads = 256) {
   void* args[] = {&prm};
   ensure_dyn_smem((const void*)kern, smem);
-  HB_CUDA(cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(threads), args, smem, st));
+  {
+    TraceSync ts(true);
+    HB_CUDA(cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(threads), args, smem, st));
+  }
   launch_counter().fetch_add(1);
   if (sync_debug_enabled()) debug_sync_after_launch("coop", grid);
 }
@@ -32,6 +35,7 @@ int clampi(int64_t v, int lo, int hi) { return (int)std::max<int64_t>(lo, std::m
 
 void sync_to_host(hb_context* c, const void* dsrc, void* hdst, size_t bytes) {
   HB_CUDA(cudaMemcpyAsync(c->pinned, dsrc, bytes, cudaMemcpyDeviceToHost, c->stream));
+  TraceSync ts;
   HB_CUDA(cudaStreamSynchronize(c->stream));
   std::memcpy(hdst, c->pinned, bytes);
 }
@@ -368,8 +372,11 @@ void two_stage_bidiag(hb_context* c, double* Mk, int64_t ldm, int64_t k, double*
   if (k > 1) {
     int* prog = ws<int>(c, B_PROG, (size_t)k);
     HB_CUDA(cudaMemsetAsync(prog, 0, sizeof(int) * k, st));
-    int per_sm = 0;
-    HB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bulge_chase_kernel, 256, 0));
+    static const int per_sm = [] {
+      int v = 0;
+      HB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, bulge_chase_kernel, 256, 0));
+      return v;
+    }();
     const int G = clampi(k - 1, 1, std::max(1, std::min(per_sm, 8)) * c->coop_sms);
     int kb = kBand;
     int64_t kk = k;
@@ -614,7 +621,10 @@ void rank_matrix_inplace(hb_context* c, double* A, int64_t m, int64_t n, int64_t
                                   (size_t)j, cudaMemcpyDeviceToDevice, st));
         std::vector<double> hd((size_t)j);
         HB_CUDA(cudaMemcpyAsync(hd.data(), dg, sizeof(double) * j, cudaMemcpyDeviceToHost, st));
-        HB_CUDA(cudaStreamSynchronize(st));
+        {
+          TraceSync ts;
+          HB_CUDA(cudaStreamSynchronize(st));
+        }
         const double thr = tol_min * sigma1_est;
         int64_t ph = -1;
         for (int64_t i = 0; i < j; ++i)
@@ -704,7 +714,10 @@ void rank_matrix_inplace(hb_context* c, double* A, int64_t m, int64_t n, int64_t
                                : 0.2 * eta_cur;
   }
   HB_CUDA(cudaEventRecord(c->ev[3], st));
-  HB_CUDA(cudaEventSynchronize(c->ev[3]));
+  {
+    TraceSync ts;
+    HB_CUDA(cudaEventSynchronize(c->ev[3]));
+  }
   float f_ms = 0.f, c_ms = 0.f;
   HB_CUDA(cudaEventElapsedTime(&f_ms, c->ev[1], c->ev[2]));
   HB_CUDA(cudaEventElapsedTime(&c_ms, c->ev[2], c->ev[3]));
@@ -787,6 +800,10 @@ void context_init(hb_context* c, int device) {
   HB_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
   HB_CUDA(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
   c->coop_sms = c->num_sms;
+  {
+    size_t free_b = 0;
+    HB_CUDA(cudaMemGetInfo(&free_b, &c->total_mem));
+  }
   if (const char* e = getenv("HB_SPECTRAL")) c->spectral = atoi(e) != 0;  // experiments / sweeps
   cudaMemPool_t pool;
   HB_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
