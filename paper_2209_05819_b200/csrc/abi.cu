@@ -620,7 +620,7 @@ hb_status hb_sweep_ex(const hb_problem* probs, int64_t n, const int32_t* devices
           subs.push_back(sc);
         }
         // stream 0 runs the costliest small problem (the critical path of the group) at high
-        // stream priority with half of the SMs for its cooperative grids; the others share the
+        // stream priority with 35% of the SMs for its cooperative grids; the others share the
         // rest (caps sum to <= num_sms, so co-resident barriers cannot deadlock)
         int lo = 0, hi = 0;
         cudaDeviceGetStreamPriorityRange(&lo, &hi);
@@ -630,7 +630,7 @@ hb_status hb_sweep_ex(const hb_problem* probs, int64_t n, const int32_t* devices
         }
         static const double crit_share = [] {  // SM share of the critical stream's coop grids
           const char* e = getenv("HB_CRIT_SHARE");
-          const double v = e ? atof(e) : 0.5;
+          const double v = e ? atof(e) : 0.35;
           return v < 0.1 ? 0.1 : (v > 0.9 ? 0.9 : v);
         }();
         const int half = std::max(1, (int)(c->num_sms * crit_share));
