@@ -222,7 +222,8 @@ def golden_map():
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=None,
+                    help="timed steps (default 5; 1 for the two-minute sweep workload)")
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c1", choices=["c0", "c1", "c2", "c3", "sweep"],
@@ -232,6 +233,8 @@ def main():
                     help="CPU baseline sample: the workload's problems with N <= this")
     ap.add_argument("--details", default="", help="write per-problem results/stats JSON here")
     args = ap.parse_args()
+    if args.steps is None:
+        args.steps = 1 if args.workload == "sweep" else 5
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
