@@ -5,6 +5,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstring>
+#include <condition_variable>
 #include <mutex>
 #include <numeric>
 #include <thread>
@@ -520,9 +521,12 @@ void hb_sweep_release(void) {
   for (auto* c : cs) hb_context_destroy(c);
 }
 
-static constexpr int64_t kSmallN = 16384;   // problems up to this N ...
-static constexpr double kSmallRank = 1000.0; // ... and this predicted rank share the GPU ...
-static constexpr int kSubStreams = 4;      // ... on this many concurrent streams (HB_SUBSTREAMS)
+static constexpr int64_t kSmallN = 16384;   // above this N a problem is "big" (K >= 2 GB)
+static constexpr double kSmallRank = 1000.0; // HB_SOLO_BIG=1 only: solo above this predicted rank
+static constexpr int kSubStreams = 4;      // concurrent streams per GPU (HB_SUBSTREAMS)
+static constexpr int kMaxBig = 3;          // at most this many N > kSmallN problems in flight
+static constexpr double kSoloFrac = 0.3;   // K above this share of device memory runs alone
+static constexpr size_t kTrimBytes = size_t(4) << 30;  // after a big problem keep buffers <= this
 
 static int sub_streams() {
   static const int n = [] {
@@ -566,15 +570,36 @@ hb_status hb_sweep_ex(const hb_problem* probs, int64_t n, const int32_t* devices
     std::stable_sort(mine.begin(), mine.end(), [&](int64_t a, int64_t b) { return cost[a] > cost[b]; });
     cudaSetDevice(c->device);
     cudaEventRecord(c->ev[5], c->stream);
-    // Large problems one at a time with the whole GPU; then the small ones (N <= kSmallN and
-    // predicted rank <= kSmallRank: latency-bound, few blocks) on
-    // kSubStreams concurrent streams, each capped to 1/kSubStreams of the SMs for its
-    // cooperative grids (their sum always fits, so co-resident barriers cannot deadlock).
-    std::vector<int64_t> small;
+    // All problems share kSubStreams concurrent streams fed from one queue in cost order (LPT),
+    // each stream's cooperative grids capped to a share of the SMs (the caps sum to <= #SMs, so
+    // co-resident grid barriers cannot deadlock).  Big problems (N > kSmallN: K alone >= 2 GB)
+    // are admitted at most kMaxBig at a time — three N = 65536 problems with their certification
+    // workspaces take ~135 GB — and a stream that finished one frees its big buffers.  Only a
+    // problem whose K alone exceeds kSoloFrac of device memory runs by itself, first, with the
+    // whole GPU.  HB_SOLO_BIG=1 restores the round-1 policy (every problem with N > HB_SMALL_N
+    // or predicted rank > HB_SMALL_RANK solo), for comparisons.
+    static const int64_t small_n = [] {
+      const char* e = getenv("HB_SMALL_N");
+      return e ? (int64_t)atoll(e) : kSmallN;
+    }();
+    static const double small_rank = [] {
+      const char* e = getenv("HB_SMALL_RANK");
+      return e ? atof(e) : kSmallRank;
+    }();
+    static const bool solo_big = [] {
+      const char* e = getenv("HB_SOLO_BIG");
+      return e && atoi(e) != 0;
+    }();
+    auto np_of = [&](int64_t i) { return std::max(probs[i].pair.n_target, probs[i].pair.n_source); };
+    auto is_big = [&](int64_t i) { return np_of(i) > small_n; };
+    std::vector<int64_t> small;  // the shared queue, costliest first
     for (int64_t i : mine) {
       const hb_problem& p = probs[i];
-      const int64_t np = std::max(p.pair.n_target, p.pair.n_source);
-      if (np <= kSmallN && predicted_rank(p.pair.target.d, p.pair.d_prime, np) <= kSmallRank) {
+      const int64_t np = np_of(i);
+      const double k_bytes = 8.0 * (double)hb::round_up(p.pair.n_target, 8) * (double)p.pair.n_source;
+      const bool solo = solo_big ? (np > small_n || predicted_rank(p.pair.target.d, p.pair.d_prime, np) > small_rank)
+                                 : k_bytes > kSoloFrac * (double)c->total_mem;
+      if (!solo) {
         small.push_back(i);
         continue;
       }
@@ -596,14 +621,39 @@ hb_status hb_sweep_ex(const hb_problem* probs, int64_t n, const int32_t* devices
       }();
       const int nback = std::min(back_env, nsub - 1);
       std::mutex q_mu;
+      std::condition_variable q_cv;
       int64_t q_front = 0, q_back = (int64_t)small.size() - 1;
-      auto take = [&](bool from_back) -> int64_t {
-        std::lock_guard<std::mutex> lk(q_mu);
-        if (q_front > q_back) return -1;
-        return from_back ? q_back-- : q_front++;
+      int big_running = 0;
+      // take the next problem from the preferred end; a big one only while fewer than kMaxBig
+      // are running (else the other end's problem if it is not big, else wait — or, when
+      // `wait` is false, return -2)
+      auto take_ex = [&](bool from_back, bool wait) -> int64_t {
+        std::unique_lock<std::mutex> lk(q_mu);
+        for (;;) {
+          if (q_front > q_back) return -1;
+          const int64_t a = from_back ? q_back : q_front, b = from_back ? q_front : q_back;
+          for (int64_t idx : {a, b}) {
+            if (is_big(small[idx]) && big_running >= kMaxBig) continue;
+            if (is_big(small[idx])) big_running++;
+            if (idx == q_front) q_front++;
+            else q_back--;
+            return idx;
+          }
+          if (!wait) return -2;
+          q_cv.wait(lk);
+        }
+      };
+      auto take = [&](bool from_back) { return take_ex(from_back, true); };
+      auto done_big = [&](int64_t q) {
+        if (!is_big(small[q])) return;
+        {
+          std::lock_guard<std::mutex> lk(q_mu);
+          big_running--;
+        }
+        q_cv.notify_all();
       };
       std::vector<int64_t> first_q(nsub);  // stream 0 starts with the costliest problem
-      for (int s = 0; s < nsub; ++s) first_q[s] = take(s >= nsub - nback);
+      for (int s = 0; s < nsub; ++s) first_q[s] = take_ex(s >= nsub - nback, false);
       std::vector<std::thread> sth;
       std::mutex sub_mu;
       std::vector<std::string> trace_lines;
@@ -611,8 +661,13 @@ hb_status hb_sweep_ex(const hb_problem* probs, int64_t n, const int32_t* devices
       auto sub_worker = [&](int s) {
         hb_status ss = HB_OK;
         hb_context* sc = cached_context(devices[w], 1000 + slot[w] * 16 + s, &ss);
+        const bool from_back = s >= nsub - nback;
+        int64_t q0 = first_q[s] == -2 ? take(from_back) : first_q[s];
         if (!sc) {
-          for (int64_t q = first_q[s]; q >= 0; q = take(s >= nsub - nback)) st[small[q]] = ss;
+          for (int64_t q = q0; q >= 0; q = take(from_back)) {
+            st[small[q]] = ss;
+            done_big(q);
+          }
           return;
         }
         {
@@ -639,8 +694,7 @@ hb_status hb_sweep_ex(const hb_problem* probs, int64_t n, const int32_t* devices
         sc->profiling = c->profiling;
         cudaStreamWaitEvent(sc->stream, ready, 0);
         static const bool timeline = getenv("HB_TIMELINE") != nullptr;
-        const bool from_back = s >= nsub - nback;
-        for (int64_t q = first_q[s]; q >= 0; q = take(from_back)) {
+        for (int64_t q = q0; q >= 0; q = take(from_back)) {
           const hb_problem& p = probs[small[q]];
           cudaEvent_t e0 = nullptr, e1 = nullptr;
           if (timeline) {
@@ -652,6 +706,13 @@ hb_status hb_sweep_ex(const hb_problem* probs, int64_t n, const int32_t* devices
           const hb::HostTrace h0 = hb::host_trace();
           const double t0 = ht ? hb::host_now() : 0.0;
           st[small[q]] = hb_rank(sc, &p.kernel, &p.pair, p.tols, p.ntol, out + offset[small[q]]);
+          if (is_big(small[q])) {  // give the pool back its big buffers before the cap opens
+            try {
+              hb::context_trim(sc, kTrimBytes);
+            } catch (const hb::Error&) {
+            }
+            done_big(q);
+          }
           if (ht) {
             const hb::HostTrace& h1 = hb::host_trace();
             char buf[256];

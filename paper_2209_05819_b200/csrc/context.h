@@ -106,6 +106,8 @@ void rank_matrix_inplace(hb_context* c, double* A, int64_t m, int64_t n, int64_t
                          float* cert_ms);
 void context_init(hb_context* c, int device);
 void context_set_priority(hb_context* c, int prio);
+// free (stream-ordered, back to the device pool) every workspace buffer larger than keep_bytes
+void context_trim(hb_context* c, size_t keep_bytes);
 void context_free(hb_context* c);
 
 }  // namespace hb

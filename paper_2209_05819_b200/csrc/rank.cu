@@ -832,6 +832,16 @@ void context_set_priority(hb_context* c, int prio) {
   c->priority = prio;
 }
 
+void context_trim(hb_context* c, size_t keep_bytes) {
+  HB_CUDA(cudaSetDevice(c->device));
+  for (auto& b : c->bufs)
+    if (b.p && b.cap > keep_bytes) {
+      HB_CUDA(cudaFreeAsync(b.p, c->stream));
+      b.p = nullptr;
+      b.cap = 0;
+    }
+}
+
 void context_free(hb_context* c) {
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
