@@ -624,6 +624,10 @@ hb_status hb_sweep_ex(const hb_problem* probs, int64_t n, const int32_t* devices
       std::condition_variable q_cv;
       int64_t q_front = 0, q_back = (int64_t)small.size() - 1;
       int big_running = 0;
+      static const int max_big = [] {  // HB_MAX_BIG: experiments
+        const char* e = getenv("HB_MAX_BIG");
+        return e ? std::max(1, atoi(e)) : kMaxBig;
+      }();
       // take the next problem from the preferred end; a big one only while fewer than kMaxBig
       // are running (else the other end's problem if it is not big, else wait — or, when
       // `wait` is false, return -2)
@@ -633,7 +637,7 @@ hb_status hb_sweep_ex(const hb_problem* probs, int64_t n, const int32_t* devices
           if (q_front > q_back) return -1;
           const int64_t a = from_back ? q_back : q_front, b = from_back ? q_front : q_back;
           for (int64_t idx : {a, b}) {
-            if (is_big(small[idx]) && big_running >= kMaxBig) continue;
+            if (is_big(small[idx]) && big_running >= max_big) continue;
             if (is_big(small[idx])) big_running++;
             if (idx == q_front) q_front++;
             else q_back--;
