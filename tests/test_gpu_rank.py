@@ -237,6 +237,21 @@ def test_sweep_matches_single_calls(ctx, hb):
     assert st == [0, 5]
 
 
+def test_sweep_big_problem_queue(ctx, hb):
+    """Five big problems (N > 16384: at most 3 in flight on the shared queue, big buffers trimmed
+    after each) mixed with small ones: every status OK and every rank equal to the single call's."""
+    spec = [(1, None, "exp_neg_r", 20000), (2, None, "log_r", 18000), (1, 0, "exp_neg_r", 17000),
+            (2, None, "exp_neg_r", 16500), (1, None, "one_over_r", 24000),
+            (2, 1, "log_r", 1000), (3, None, "one_over_r", 2000), (1, 0, "log_r", 4000)]
+    probs = [hb.make_problem(k, d, dp, n, [1e-12]) for (d, dp, k, n) in spec]
+    res, st = hb.sweep(probs, [0])
+    assert st == [0] * len(probs)
+    for p, rr in zip(probs, res):
+        single = ctx.rank(p.kernel, p.pair, list(p.tols[: p.ntol]))
+        assert [x.rank for x in rr] == [x.rank for x in single]
+        assert rr[0].certificate == 1
+
+
 def test_profiling_stats(ctx, hb):
     ctx.set_profiling(True)
     ctx.rank(hb.make_kernel("exp_neg_r"), hb.make_pair(4, 3, 2000, hb.UNIFORM, 1), [1e-12])
