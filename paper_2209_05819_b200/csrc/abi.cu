@@ -526,7 +526,7 @@ static constexpr double kSmallRank = 1000.0; // HB_SOLO_BIG=1 only: solo above t
 static constexpr int kSubStreams = 4;      // concurrent streams per GPU (HB_SUBSTREAMS)
 static constexpr int kMaxBig = 3;          // at most this many N > kSmallN problems in flight
 static constexpr double kSoloFrac = 0.3;   // K above this share of device memory runs alone
-static constexpr size_t kTrimBytes = size_t(4) << 30;  // after a big problem keep buffers <= this
+static constexpr size_t kTrimBytes = size_t(16) << 30;  // after a big problem keep buffers <= this
 
 static int sub_streams() {
   static const int n = [] {
