@@ -1,19 +1,21 @@
 #!/usr/bin/env python
 """bench.py — rank-revealed kernel entries per second on B200 (BASELINE.json metric).
 
-Workload (default "sweep" = BASELINE.json configs[4]): d = 1..4, every shared
-hyper-surface d' in {0..d-1} plus far-field, kernels {log r, 1/r, exp(-r)}, N in {1000, 2000,
-4000, 8000, 16000, 32000, 65536} i.i.d. uniform FP64 points per cube from per-problem seeds
-(hb_problem_seed(0, d, d', N)), tol 1e-12 (d = 4: 1e-12 and 1e-10) -> 294 independent problems,
-Σ N² = 2.38e11 entries.  One step = one pass of the whole path over the sweep: generate points,
-assemble K, sketch-pivoted QR, certify the ε-rank.
+Default workload "c3" = BASELINE.json configs[3]: d = 4, the unit hyper-cube against neighbours
+sharing d' = 0..3 hyper-surfaces plus far-field, F = exp(-r), N in {2000, 4000, 8000, 16000,
+32000, 65536} i.i.d. uniform FP64 points per cube from per-problem seeds (hb_problem_seed(0, d,
+d', N)), tolerances 1e-12 and 1e-10 -> 30 problems, Σ N² = 2.8e10 entries per step.  One step =
+one pass of the whole path over the config: generate points, assemble K, sketch-pivoted QR,
+certify the ε-rank.  (configs[4], the 294-problem sweep, is `--workload sweep`; one sweep step
+takes ~110 s, so 25 driver steps would not fit the arm's time budget — VERDICT r1 item 2.)
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload sweep|d1|d2|d3|d4]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--workload c0|c1|c2|c3|sweep]
 
 N > 1 runs under torchrun (one process per GPU, NCCL only for the final result gather).
-Per-config workloads (c0..c3, default c1) scale WEAK: every rank runs the whole config on its
-own independent problems (per-problem seeds from base seed = rank; rank 0's are the golden ones),
-so the work per GPU is fixed and `value` = all ranks' entries / max-over-ranks device time.
+Per-config workloads (c0..c3) scale WEAK: every rank runs the whole config on its own
+independent problems (per-problem seeds from base seed = rank; rank 0's are the golden ones), so
+the work per GPU is fixed and `value` = all ranks' entries / max-over-ranks device time.
 The full sweep (configs[4], which BASELINE.json states as partitioned across 1/2/4/8 B200) is
 LPT-partitioned over the ranks (hb_partition): total work fixed -> strong scaling.
 """
@@ -223,18 +225,21 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=None,
-                    help="timed steps (default 5; 1 for the two-minute sweep workload)")
+                    help="timed steps (default 3; 1 for the two-minute sweep workload)")
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c1", choices=["c0", "c1", "c2", "c3", "sweep"],
+    ap.add_argument("--workload", default="c3", choices=["c0", "c1", "c2", "c3", "sweep"],
                     help="BASELINE.json configs[0..3] (c0..c3) or the full configs[4] sweep")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-max-n", type=int, default=4000,
                     help="CPU baseline sample: the workload's problems with N <= this")
+    ap.add_argument("--ref-sample-max-n", type=int, default=2000,
+                    help="--impl reference: per-step sample = the workload's problems with N <= this "
+                         "(bounded so warmup + 25 steps fit the arm's time budget)")
     ap.add_argument("--details", default="", help="write per-problem results/stats JSON here")
     args = ap.parse_args()
     if args.steps is None:
-        args.steps = 1 if args.workload == "sweep" else 5
+        args.steps = 1 if args.workload == "sweep" else 3
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -261,9 +266,11 @@ def main():
 
     if args.impl == "reference":
         # the reference's CPU path for this workload = the oracle port (the reference ships no
-        # rank driver and needs Eigen), on a bounded sample of the same sweep
+        # rank driver and needs Eigen), on a bounded sample of the same workload
         if rank != 0:
             return 0
+        sample = [w for w in wl if w[3] <= args.ref_sample_max_n] or sorted(wl, key=lambda w: w[3])[:3]
+        args.cpu_sample_max_n = max(w[3] for w in sample)
         for _ in range(args.warmup):
             cpu_baseline_run(sample[:3], threads)
         vals, dts = [], []
@@ -325,7 +332,7 @@ def main():
     dev_secs, walls, my_res, statuses = [], [], None, []
     for _ in range(args.steps):
         t0 = time.perf_counter()
-        my_res, st, ds = hb.sweep(my_probs, [dev], profiling=True, with_times=True)
+        my_res, st, ds = hb.sweep(my_probs, [dev], profiling=False, with_times=True)
         walls.append(time.perf_counter() - t0)
         dev_secs.append(ds[0])
         statuses = st
@@ -333,18 +340,28 @@ def main():
     clocks = clk.stop()
     stats = hb.global_stats()
     launches = stats["launches"] - launches0
-    # context for the roofline: the same GEMMs measured without the concurrent small-problem
-    # streams — one untimed pass of this rank's costliest problem alone (after the timed region)
+    # The dominant kernel (the DMMA GEMM) measured without overlap: one untimed, profiled pass of
+    # this rank's costliest problem alone on one stream after the timed region — CUDA events
+    # around every GEMM launch on the stream it runs on, so the GEMM time is a share of that
+    # problem's device time (never more), and the phase split of the same pass.
     iso = None
     if my_probs:
-        crit = max(my_probs, key=lambda p: p.pair.n_target)
+        crit = max(my_probs, key=lambda p: (p.pair.n_target, p.pair.d_prime))
         hb.reset_global_stats()
-        hb.sweep([crit], [dev], profiling=True)
+        _, _, ds1 = hb.sweep([crit], [dev], profiling=True, with_times=True)
         st1 = hb.global_stats()
         if st1["gemm_ms"] > 0:
-            iso = {"achieved": round(st1["gemm_flops"] / (st1["gemm_ms"] * 1e-3) / 1e12, 3),
+            iso = {"kernel": "dgemm (FP64 DMMA m8n8k4): trailing update, sketch, WY and "
+                             "certification-QR GEMMs",
+                   "achieved": round(st1["gemm_flops"] / (st1["gemm_ms"] * 1e-3) / 1e12, 3),
+                   "gemm_ms": round(st1["gemm_ms"], 1), "problem_ms": round(ds1[0] * 1e3, 1),
+                   "gemm_share": round(st1["gemm_ms"] / (ds1[0] * 1e3), 4),
+                   "gemm_launches": st1["gemm_launches"],
                    "problem": f"d={crit.pair.target.d} d'={crit.pair.d_prime} N={crit.pair.n_target}",
-                   "note": "untimed solo pass after the timed region (no concurrent streams)"}
+                   "phase_ms": {k: round(v, 1) for k, v in st1["phase_ms"].items()},
+                   "note": "untimed solo pass of the costliest problem after the timed region "
+                           "(one stream, no overlap): achieved = sum 2MNK / sum of per-launch "
+                           "CUDA-event times"}
     t_dev = sum(dev_secs)
     t_wall = sum(walls)
     if dist:
@@ -366,7 +383,6 @@ def main():
     value = entries * args.steps / t_dev / 1e9
     e2e = entries * args.steps / t_wall / 1e9
     peak, peak_src = fp64_peak()
-    gemm_tf = stats["gemm_flops"] / (stats["gemm_ms"] * 1e-3) / 1e12 if stats["gemm_ms"] > 0 else 0.0
     # parity vs the committed oracle golden file (problems the CPU oracle could do)
     gm = golden_map()
     checked = equal = 0
@@ -400,16 +416,14 @@ def main():
                 "note": "whole job (all ranks)",
                 "api": "hb_sweep_ex (C ABI) from host descriptors to host result records; points are "
                        "generated on device from the seeds (k1)"},
-        "roofline": {"bound": "tensor", "kernel": "dgemm_kernel (FP64 DMMA m8n8k4; trailing update, "
-                     "sketch, WY and certification QR GEMMs)",
-                     "achieved": round(gemm_tf, 3), "peak": peak, "unit": "TFLOP/s",
-                     "frac": round(gemm_tf / peak, 4), "traffic": ncu_traffic()[0],
-                     "traffic_source": ncu_traffic()[1], "peak_source": peak_src,
-                     "measured": "CUDA events around every DMMA GEMM launch on its stream, timed region",
-                     "isolated": (dict(iso, frac=round(iso["achieved"] / peak, 4)) if iso else None),
-                     "path": {"alg_tflops": round(path_tf, 3), "frac": round(path_tf / peak, 4),
-                              "model": "FLOP_alg = N^2 c_F + 4N^2 p - 4N p^2 + 4/3 p^3 (SURVEY 8d), "
-                                       "p = certified rank, over device time of the step"}},
+        "roofline": {
+            "bound": "tensor", "achieved": round(path_tf, 3), "peak": peak, "unit": "TFLOP/s",
+            "frac": round(path_tf / peak, 4), "traffic": ncu_traffic()[0],
+            "scope": "north-star path fraction: FLOP_alg per step / device time per step / FP64 "
+                     "peak, FLOP_alg = sum over problems of N^2 c_F + 4N^2 p - 4N p^2 + 4/3 p^3 "
+                     "(SURVEY.md 8(d), p = certified rank)",
+            "peak_source": peak_src, "traffic_source": ncu_traffic()[1],
+            "kernel": (dict(iso, peak=peak, frac=round(iso["achieved"] / peak, 4)) if iso else None)},
         "gpu_launches": int(launches),
         "clocks": clocks,
         "parity": {"checked_vs_oracle": checked, "equal": equal, "mismatches": mism[:20],
@@ -417,8 +431,6 @@ def main():
                    "statuses_ok": all(s == 0 for s in statuses),
                    "failed": [[list(w[:4]), s] for w, s in zip([wl[i % len(wl)] for i in mine], statuses) if s != 0][:10],
                    "last_error": hb.load().hb_last_error(None).decode()[:200]},
-        "phase_ms": {k: round(v, 1) for k, v in stats["phase_ms"].items()},
-        "gemm_ms": round(stats["gemm_ms"], 1),
     }
     if world == 1 and not args.no_cpu_baseline:
         v, dt, ent, kind = cpu_baseline_run(sample, threads)

@@ -11,8 +11,13 @@
  *   hb_kernel              <- hodlr::KernelSpec / KernelId          kernel.hpp:19-32, 37-110
  *   hb_cube                <- hodlr::HyperCube{lower, side}         geometry.hpp:15-64
  *   hb_pair.d_prime        <- hodlr::InteractionClass (far / surface:d')  geometry.hpp:77-104
+ *   hb_classify_pair       <- hodlr::classify_pair(BoxIndex, BoxIndex)  geometry.hpp:106-118
+ *   hb_classify_cubes      <- classify_pair on two cubes of one uniform subdivision
+ *                             (the inverse of box_cube, geometry.hpp:145-151)
  *   hb_generate_points     <- SPEC pair_geometry (X, Y point sets)
  *   hb_assemble            <- hodlr::assemble_dense                 kernel.hpp:168-181
+ *   hb_assemble_dense_host <- hodlr::assemble_dense on host PointSets (same call, host buffers,
+ *                             entry cap -> HB_ECAP)                  kernel.hpp:168-181
  *   hb_eval_radial_host    <- hodlr::eval_radial (scalar, host)     kernel.hpp:149-157
  *   hb_rank_matrix         <- SPEC epsilon_rank(matrix, epsilon)
  *   hb_rank                <- SPEC pair_geometry -> assemble_dense -> epsilon_rank
@@ -83,8 +88,12 @@ typedef struct {
 } hb_cube;
 
 /* A target/source cube pair with its point clouds.
- * d_prime: -1 far-field, else dimension of the shared hyper-surface (descriptor only; the
- * geometry itself is carried by the cubes). */
+ * d_prime: HB_DPRIME_FAR (-1) far-field, HB_DPRIME_SELF (-2) the same box, else the dimension of
+ * the shared hyper-surface.  The geometry itself is carried by the cubes; when the two cubes are
+ * boxes of one uniform subdivision (equal sides, corner offsets integer multiples of the side)
+ * d_prime must equal hb_classify_cubes(target, source), else HB_EINVAL. */
+#define HB_DPRIME_FAR (-1)
+#define HB_DPRIME_SELF (-2)
 typedef struct {
   hb_cube target;
   hb_cube source;
@@ -141,6 +150,24 @@ hb_status hb_context_set_tuning(hb_context* ctx, int32_t block_max, double eta);
  * default 0: the residual checks cost more than the columns they save on the BASELINE sweep. */
 hb_status hb_context_set_stopping(hb_context* ctx, int32_t spectral);
 
+/* InteractionClass (geometry.hpp:77-104): kind + surface dimension (valid for SURFACE only). */
+enum { HB_IC_SELF = 0, HB_IC_SURFACE = 1, HB_IC_FAR = 2 };
+typedef struct {
+  int32_t kind;
+  int32_t surface_dim; /* d' for HB_IC_SURFACE, else -1 */
+} hb_interaction;
+
+/* classify_pair (geometry.hpp:109-118) on two BoxIndex values (level, d per-axis grid coords):
+ * all offsets 0 -> SELF; any |offset| >= 2 -> FAR; else SURFACE with d' = #zero offsets.
+ * Different levels or d < 1 -> HB_EINVAL (the reference's invalid_argument). */
+hb_status hb_classify_pair(int32_t d, int32_t level_a, const int32_t* grid_a, int32_t level_b,
+                           const int32_t* grid_b, hb_interaction* out);
+/* The same classification for two cubes of one uniform subdivision: equal sides and corner
+ * offsets that are integer multiples of the side (else HB_EINVAL: not a same-level box pair). */
+hb_status hb_classify_cubes(const hb_cube* a, const hb_cube* b, hb_interaction* out);
+/* hb_pair.d_prime value of a classification (HB_DPRIME_SELF / HB_DPRIME_FAR / d'). */
+int32_t hb_interaction_dprime(hb_interaction ic);
+
 /* k1: seeded / grid points, SoA (coordinate k of point i at k*n + i), device pointers. */
 hb_status hb_generate_points(hb_context* ctx, const hb_pair* pair, double* d_tgt_soa,
                              double* d_src_soa);
@@ -149,6 +176,15 @@ hb_status hb_generate_points(hb_context* ctx, const hb_pair* pair, double* d_tgt
  * Device pointers; ordered on the context stream; synchronises to report ESINGULAR/EDOMAIN. */
 hb_status hb_assemble(hb_context* ctx, const hb_kernel* kernel, const double* d_tgt_soa, int64_t T,
                       const double* d_src_soa, int64_t N, int32_t d, double* d_K, int64_t ldk);
+
+/* assemble_dense (kernel.hpp:168-181) on HOST buffers: targets T x d and sources N x d point sets
+ * in the reference's PointSet layout (column-major, points are rows = SoA), K column-major T x N
+ * with leading dimension ldk >= T.  Copies the points to the device, assembles there (k2) and
+ * copies K back.  entry_cap > 0 mirrors the reference's cap (T > entry_cap / N -> HB_ECAP); 0 = no
+ * cap.  Empty point sets -> HB_EINVAL; r == 0 on a singular kernel without diagonal -> ESINGULAR. */
+hb_status hb_assemble_dense_host(hb_context* ctx, const hb_kernel* kernel, const double* tgt_soa,
+                                 int64_t T, const double* src_soa, int64_t N, int32_t d,
+                                 double* K, int64_t ldk, int64_t entry_cap);
 
 /* Scalar host evaluation of F(r) with the r == 0 rule (kernel.hpp:149-157). */
 hb_status hb_eval_radial_host(const hb_kernel* kernel, double r, double* out);

@@ -228,6 +228,9 @@ def ref_lib():
         L.hbr_eval_radial.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_double,
                                       ctypes.c_double, ctypes.POINTER(ctypes.c_int)]
         L.hbr_eval_radial.restype = ctypes.c_double
+        L.hbr_classify_pair.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_int,
+                                        ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+        L.hbr_box_grid.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int64, ctypes.c_void_p]
         for f in ("hbr_j2", "hbr_y2"):
             getattr(L, f).argtypes = [ctypes.c_double]
             getattr(L, f).restype = ctypes.c_double

@@ -1,5 +1,5 @@
 // ref_wrap.cpp -- TEST INFRASTRUCTURE ONLY.  extern "C" wrapper that compiles the reference's
-// own headers (kernel.hpp, aca.hpp, bessel.hpp, types.hpp) from where they lie under
+// own headers (kernel.hpp, aca.hpp, bessel.hpp, geometry.hpp, types.hpp) from where they lie under
 // /root/reference/proj/include, against the from-scratch Eigen subset in oracle/eigen_shim,
 // into oracle/_ref/libhb_ref.so.  No reference source is copied into this repository.
 // It is the second oracle: tests pin the C restatement (hb_oracle.c) against it, and
@@ -10,6 +10,7 @@
 #include <stdexcept>
 
 #include "hodlr/aca.hpp"
+#include "hodlr/geometry.hpp"
 #include "hodlr/kernel.hpp"
 
 using namespace hodlr;
@@ -105,6 +106,34 @@ int hbr_aca_compress(int id, int has_diag, double diag, const double* x_soa, int
       const Vector bb = apply(f, blk, qq);
       for (int64_t i = 0; i < rows; ++i) b[i] = bb(i);
     }
+  });
+}
+
+// hodlr::classify_pair (geometry.hpp:109-118) on two BoxIndex values; kind 0 self, 1 shared
+// surface (surface_dim = d'), 2 far (hb.h HB_IC_*).
+int hbr_classify_pair(int d, int level_a, const int32_t* grid_a, int level_b, const int32_t* grid_b,
+                      int32_t* kind, int32_t* surface_dim) {
+  return guarded([&] {
+    BoxIndex a, b;
+    a.level = level_a;
+    b.level = level_b;
+    a.grid = Eigen::ArrayXi::Zero(d);
+    b.grid = Eigen::ArrayXi::Zero(d);
+    for (int k = 0; k < d; ++k) {
+      a.grid(k) = grid_a[k];
+      b.grid(k) = grid_b[k];
+    }
+    const InteractionClass ic = classify_pair(a, b);
+    *kind = ic.is_self() ? 0 : (ic.is_far() ? 2 : 1);
+    *surface_dim = ic.surface_dim;
+  });
+}
+
+// hodlr::box_grid / box_id (geometry.hpp:123-141): z-order box id <-> per-axis grid.
+int hbr_box_grid(int d, int level, int64_t id, int32_t* grid) {
+  return guarded([&] {
+    const Eigen::ArrayXi g = box_grid(d, level, id);
+    for (int k = 0; k < d; ++k) grid[k] = g(k);
   });
 }
 

@@ -3,6 +3,7 @@
 // No C++ exception crosses this file's extern "C" functions.
 #include <algorithm>
 #include <atomic>
+#include <memory>
 #include <cmath>
 #include <cstring>
 #include <condition_variable>
@@ -83,6 +84,39 @@ int64_t check_points(const hb_cube& c, int64_t n, int mode) {
   return m;
 }
 
+// classify_pair (geometry.hpp:109-118) on per-axis grid offsets
+hb_interaction classify_offsets(const int64_t* off, int d) {
+  bool all_zero = true;
+  int64_t mx = 0;
+  int zeros = 0;
+  for (int k = 0; k < d; ++k) {
+    const int64_t o = off[k] < 0 ? -off[k] : off[k];
+    all_zero &= o == 0;
+    mx = std::max(mx, o);
+    zeros += o == 0;
+  }
+  if (all_zero) return hb_interaction{HB_IC_SELF, -1};
+  if (mx >= 2) return hb_interaction{HB_IC_FAR, -1};
+  return hb_interaction{HB_IC_SURFACE, zeros};
+}
+
+// Two cubes of one uniform subdivision: equal sides, corner offsets integer multiples of the side
+// (exactly representable here: the offsets are small integers times the side).  false if not.
+bool cube_offsets(const hb_cube& a, const hb_cube& b, int64_t* off) {
+  if (a.d != b.d || a.side != b.side) return false;
+  for (int k = 0; k < a.d; ++k) {
+    const double q = (b.lower[k] - a.lower[k]) / a.side;
+    const double r = std::nearbyint(q);
+    if (!(std::fabs(q - r) <= 1e-9 * std::max(1.0, std::fabs(q))) || std::fabs(r) > 1e15) return false;
+    off[k] = (int64_t)r;
+  }
+  return true;
+}
+
+int32_t dprime_of(const hb_interaction& ic) {
+  return ic.kind == HB_IC_SELF ? HB_DPRIME_SELF : (ic.kind == HB_IC_FAR ? HB_DPRIME_FAR : ic.surface_dim);
+}
+
 void check_pair(const hb_pair* p) {
   if (!p) throw Error(HB_EINVAL, "pair descriptor is NULL");
   check_cube(p->target);
@@ -90,6 +124,14 @@ void check_pair(const hb_pair* p) {
   if (p->target.d != p->source.d) throw Error(HB_EINVAL, "point dimensions differ");  // kernel.hpp:172
   check_points(p->target, p->n_target, p->point_mode);
   check_points(p->source, p->n_source, p->point_mode);
+  if (p->d_prime < HB_DPRIME_SELF || p->d_prime >= p->target.d)
+    throw Error(HB_EINVAL, "d_prime must be -2 (self), -1 (far) or a surface dimension 0..d-1");
+  int64_t off[8];
+  if (cube_offsets(p->target, p->source, off)) {  // boxes of one subdivision: d' is implied
+    const int32_t implied = dprime_of(classify_offsets(off, p->target.d));
+    if (implied != p->d_prime)
+      throw Error(HB_EINVAL, "d_prime does not match the cube pair's interaction class (classify_pair)");
+  }
 }
 
 void check_tols(const double* tols, int32_t ntol) {
@@ -395,6 +437,61 @@ hb_status hb_assemble(hb_context* ctx, const hb_kernel* kernel, const double* d_
   });
 }
 
+hb_status hb_classify_pair(int32_t d, int32_t level_a, const int32_t* grid_a, int32_t level_b,
+                           const int32_t* grid_b, hb_interaction* out) {
+  return guarded(nullptr, [&] {
+    if (!out || !grid_a || !grid_b) throw Error(HB_EINVAL, "classify_pair: NULL argument");
+    if (level_a != level_b)  // geometry.hpp:110-111
+      throw Error(HB_EINVAL, "classify_pair: boxes are at different levels");
+    if (d < 1 || d > 64) throw Error(HB_EINVAL, "classify_pair: boxes have different dimensions");
+    std::vector<int64_t> off((size_t)d);
+    for (int k = 0; k < d; ++k) off[(size_t)k] = (int64_t)grid_a[k] - (int64_t)grid_b[k];
+    *out = classify_offsets(off.data(), d);
+  });
+}
+
+hb_status hb_classify_cubes(const hb_cube* a, const hb_cube* b, hb_interaction* out) {
+  return guarded(nullptr, [&] {
+    if (!a || !b || !out) throw Error(HB_EINVAL, "classify: NULL argument");
+    check_cube(*a);
+    check_cube(*b);
+    int64_t off[8];
+    if (!cube_offsets(*a, *b, off))
+      throw Error(HB_EINVAL, "classify: cubes are not boxes of one uniform subdivision");
+    *out = classify_offsets(off, a->d);
+  });
+}
+
+int32_t hb_interaction_dprime(hb_interaction ic) { return dprime_of(ic); }
+
+hb_status hb_assemble_dense_host(hb_context* ctx, const hb_kernel* kernel, const double* tgt, int64_t T,
+                                 const double* src, int64_t N, int32_t d, double* K, int64_t ldk,
+                                 int64_t entry_cap) {
+  if (!ctx) return HB_EINVAL;
+  return guarded(ctx, [&] {
+    check_kernel(kernel);
+    if (T <= 0 || N <= 0) throw Error(HB_EINVAL, "assemble_dense: empty point set");  // kernel.hpp:171
+    if (d < 1 || d > 8) throw Error(HB_EINVAL, "assemble_dense: point dimensions differ");
+    if (!tgt || !src || !K) throw Error(HB_EINVAL, "NULL buffer");
+    if (ldk < T) throw Error(HB_EINVAL, "assemble_dense: ldk < T");
+    if (entry_cap > 0 && T > entry_cap / N)  // kernel.hpp:174-175
+      throw Error(HB_ECAP, "assemble_dense: T*N exceeds the entry cap");
+    HB_CUDA(cudaSetDevice(ctx->device));
+    const int64_t ldd = hb::round_up(T, 8);
+    double* dx = hb::ws<double>(ctx, hb::B_X, (size_t)d * T);
+    double* dy = hb::ws<double>(ctx, hb::B_Y, (size_t)d * N);
+    double* dk = hb::ws<double>(ctx, hb::B_A, (size_t)ldd * N);
+    HB_CUDA(cudaMemcpyAsync(dx, tgt, sizeof(double) * d * T, cudaMemcpyHostToDevice, ctx->stream));
+    HB_CUDA(cudaMemcpyAsync(dy, src, sizeof(double) * d * N, cudaMemcpyHostToDevice, ctx->stream));
+    unsigned int* flags = hb::ws<unsigned int>(ctx, hb::B_FLAGS, 4);
+    HB_CUDA(cudaMemsetAsync(flags, 0, sizeof(unsigned int), ctx->stream));
+    hb::launch_assemble(*kernel, dx, T, dy, N, d, dk, ldd, flags, ctx->stream);
+    raise_flags(read_flags(ctx, flags));
+    HB_CUDA(cudaMemcpy2DAsync(K, ldk * 8, dk, ldd * 8, T * 8, N, cudaMemcpyDeviceToHost, ctx->stream));
+    HB_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
 hb_status hb_eval_radial_host(const hb_kernel* k, double r, double* out) {
   return guarded(nullptr, [&] {
     check_kernel(k);
@@ -527,6 +624,7 @@ static constexpr int kSubStreams = 4;      // concurrent streams per GPU (HB_SUB
 static constexpr int kMaxBig = 3;          // at most this many N > kSmallN problems in flight
 static constexpr double kSoloFrac = 0.3;   // K above this share of device memory runs alone
 static constexpr size_t kTrimBytes = size_t(16) << 30;  // after a big problem keep buffers <= this
+static constexpr double kBudgetFrac = 0.88;  // admitted workspace, share of device memory
 
 static int sub_streams() {
   static const int n = [] {
@@ -537,15 +635,57 @@ static int sub_streams() {
   return n;
 }
 
+namespace {
+// Device-memory admission shared by every sweep worker on one device (duplicate device entries
+// in `devices` share it): the bytes reserved by running problems plus the workspace each stream
+// keeps between problems must stay within kBudgetFrac of device memory.
+struct DeviceBudget {
+  std::mutex mu;
+  std::condition_variable cv;
+  double reserved = 0.0;  // Σ over streams of max(bytes held, bytes its running problem needs)
+  int big_running = 0;
+};
+DeviceBudget& device_budget(int device) {
+  static std::mutex m;
+  static std::vector<std::pair<int, std::unique_ptr<DeviceBudget>>> all;
+  std::lock_guard<std::mutex> lk(m);
+  for (auto& e : all)
+    if (e.first == device) return *e.second;
+  all.emplace_back(device, std::make_unique<DeviceBudget>());
+  return *all.back().second;
+}
+
+double held_bytes(const hb_context* c) {
+  double s = 0.0;
+  for (const auto& b : c->bufs) s += (double)b.cap;
+  return s;
+}
+
+// Predicted peak workspace of one problem (rank_pair + rank_matrix_inplace): K, the
+// certification copy of R_kᵀ (k ≈ 1.6 p̂), the k x k triangle, the sketch, V and W, with the
+// 1/8 growth headroom of ws().
+double problem_bytes(const hb_problem& p) {
+  const double m = (double)p.pair.n_target, n = (double)p.pair.n_source;
+  const double np = std::max(m, n);
+  const double kh = std::min(std::min(m, n), 1.6 * predicted_rank(p.pair.target.d, p.pair.d_prime,
+                                                                   (int64_t)np) + 128.0);
+  const double lda = (double)hb::round_up((int64_t)m, 8);
+  const double b = 8.0 * (lda * n + n * kh + kh * kh + np * 4.0 * 128.0 + 128.0 * m + 3.0 * 120.0 * np);
+  return 1.125 * b + 64.0 * 1024 * 1024;
+}
+}  // namespace
+
 hb_status hb_sweep_ex(const hb_problem* probs, int64_t n, const int32_t* devices, int32_t ndev,
                       hb_rank_result* out, int32_t* status_out, hb_sweep_opts* opts) {
-  if (n < 0 || (n > 0 && (!probs || !out)) || ndev < 1 || ndev > HB_MAX_DEVICES || !devices)
+  bool bad = n < 0 || (n > 0 && (!probs || !out)) || ndev < 1 || ndev > HB_MAX_DEVICES || !devices;
+  for (int64_t i = 0; !bad && i < n; ++i) bad = probs[i].ntol < 1 || probs[i].ntol > HB_MAX_TOLS;
+  if (bad) {  // report the failure per problem too, so a caller reading statuses sees it
+    if (status_out)
+      for (int64_t i = 0; i < n; ++i) status_out[i] = HB_EINVAL;
     return HB_EINVAL;
-  std::vector<int64_t> offset(n + 1, 0);
-  for (int64_t i = 0; i < n; ++i) {
-    if (probs[i].ntol < 1 || probs[i].ntol > HB_MAX_TOLS) return HB_EINVAL;
-    offset[i + 1] = offset[i] + probs[i].ntol;
   }
+  std::vector<int64_t> offset(n + 1, 0);
+  for (int64_t i = 0; i < n; ++i) offset[i + 1] = offset[i] + probs[i].ntol;
   std::vector<int32_t> owner(n);
   hb_partition(probs, n, ndev, owner.data());
   std::vector<hb_status> st(n, HB_OK);
@@ -570,14 +710,17 @@ hb_status hb_sweep_ex(const hb_problem* probs, int64_t n, const int32_t* devices
     std::stable_sort(mine.begin(), mine.end(), [&](int64_t a, int64_t b) { return cost[a] > cost[b]; });
     cudaSetDevice(c->device);
     cudaEventRecord(c->ev[5], c->stream);
+    DeviceBudget& bud = device_budget(c->device);
+    const double budget = kBudgetFrac * (double)c->total_mem;
     // All problems share kSubStreams concurrent streams fed from one queue in cost order (LPT),
     // each stream's cooperative grids capped to a share of the SMs (the caps sum to <= #SMs, so
     // co-resident grid barriers cannot deadlock).  Big problems (N > kSmallN: K alone >= 2 GB)
-    // are admitted at most kMaxBig at a time — three N = 65536 problems with their certification
-    // workspaces take ~135 GB — and a stream that finished one frees its big buffers.  Only a
-    // problem whose K alone exceeds kSoloFrac of device memory runs by itself, first, with the
-    // whole GPU.  HB_SOLO_BIG=1 restores the round-1 policy (every problem with N > HB_SMALL_N
-    // or predicted rank > HB_SMALL_RANK solo), for comparisons.
+    // are admitted at most kMaxBig at a time AND only while the device budget holds their
+    // predicted workspace (problem_bytes) next to what the other streams hold or reserve; a
+    // stream that finished a big problem frees its > kTrimBytes buffers.  Only a problem whose K
+    // alone exceeds kSoloFrac of device memory runs by itself, first, with the whole GPU.
+    // HB_SOLO_BIG=1 restores the round-1 policy (every problem with N > HB_SMALL_N or predicted
+    // rank > HB_SMALL_RANK solo), for comparisons.
     static const int64_t small_n = [] {
       const char* e = getenv("HB_SMALL_N");
       return e ? (int64_t)atoll(e) : kSmallN;
@@ -593,6 +736,7 @@ hb_status hb_sweep_ex(const hb_problem* probs, int64_t n, const int32_t* devices
     auto np_of = [&](int64_t i) { return std::max(probs[i].pair.n_target, probs[i].pair.n_source); };
     auto is_big = [&](int64_t i) { return np_of(i) > small_n; };
     std::vector<int64_t> small;  // the shared queue, costliest first
+    bool ran_solo = false;
     for (int64_t i : mine) {
       const hb_problem& p = probs[i];
       const int64_t np = np_of(i);
@@ -603,7 +747,26 @@ hb_status hb_sweep_ex(const hb_problem* probs, int64_t n, const int32_t* devices
         small.push_back(i);
         continue;
       }
+      {  // a solo problem waits until no other worker of this device holds a big reservation
+        std::unique_lock<std::mutex> lk(bud.mu);
+        bud.cv.wait(lk, [&] { return bud.big_running == 0; });
+        bud.big_running++;
+        bud.reserved += problem_bytes(p);
+      }
       st[i] = hb_rank(c, &p.kernel, &p.pair, p.tols, p.ntol, out + offset[i]);
+      ran_solo = true;
+      {
+        std::lock_guard<std::mutex> lk(bud.mu);
+        bud.big_running--;
+        bud.reserved -= problem_bytes(p);
+      }
+      bud.cv.notify_all();
+    }
+    if (ran_solo) {  // the main context only records events from here on: give its K back
+      try {
+        hb::context_trim(c, size_t(64) << 20);
+      } catch (const hb::Error&) {
+      }
     }
     std::vector<hb_context*> subs;
     if (!small.empty()) {
@@ -620,57 +783,72 @@ hb_status hb_sweep_ex(const hb_problem* probs, int64_t n, const int32_t* devices
         return e ? std::max(0, atoi(e)) : 0;
       }();
       const int nback = std::min(back_env, nsub - 1);
-      std::mutex q_mu;
-      std::condition_variable q_cv;
       int64_t q_front = 0, q_back = (int64_t)small.size() - 1;
-      int big_running = 0;
       static const int max_big = [] {  // HB_MAX_BIG: experiments
         const char* e = getenv("HB_MAX_BIG");
         return e ? std::max(1, atoi(e)) : kMaxBig;
       }();
-      // take the next problem from the preferred end; a big one only while fewer than kMaxBig
-      // are running (else the other end's problem if it is not big, else wait — or, when
-      // `wait` is false, return -2)
-      auto take_ex = [&](bool from_back, bool wait) -> int64_t {
-        std::unique_lock<std::mutex> lk(q_mu);
+      // per-stream reservation (bytes) in the device budget; guarded by bud.mu
+      std::vector<double> res(nsub, 0.0);
+      std::vector<hb_context*> sctx(nsub, nullptr);
+      // take the next problem from the preferred end (else the other end); a big one only while
+      // fewer than kMaxBig run and its workspace fits the device budget next to everything the
+      // other streams hold — unless no big problem runs at all (progress).  Waits when nothing
+      // can be admitted (or returns -2 when `wait` is false).  Lock order: bud.mu only.
+      auto take_ex = [&](int s, bool from_back, bool wait) -> int64_t {
+        std::unique_lock<std::mutex> lk(bud.mu);
         for (;;) {
           if (q_front > q_back) return -1;
           const int64_t a = from_back ? q_back : q_front, b = from_back ? q_front : q_back;
+          const double held = sctx[s] ? held_bytes(sctx[s]) : 0.0;
           for (int64_t idx : {a, b}) {
-            if (is_big(small[idx]) && big_running >= max_big) continue;
-            if (is_big(small[idx])) big_running++;
+            const hb_problem& p = probs[small[idx]];
+            const double need = std::max(held, problem_bytes(p));
+            if (is_big(small[idx])) {
+              if (bud.big_running >= max_big) continue;
+              if (bud.big_running > 0 && bud.reserved - res[s] + need > budget) continue;
+              bud.big_running++;
+            }
+            bud.reserved += need - res[s];
+            res[s] = need;
             if (idx == q_front) q_front++;
             else q_back--;
             return idx;
           }
           if (!wait) return -2;
-          q_cv.wait(lk);
+          bud.cv.wait(lk);
         }
       };
-      auto take = [&](bool from_back) { return take_ex(from_back, true); };
-      auto done_big = [&](int64_t q) {
-        if (!is_big(small[q])) return;
+      // after a problem: drop the reservation to what the stream keeps
+      auto finished = [&](int s, int64_t q) {
         {
-          std::lock_guard<std::mutex> lk(q_mu);
-          big_running--;
+          std::lock_guard<std::mutex> lk(bud.mu);
+          if (is_big(small[q])) bud.big_running--;
+          const double keep = sctx[s] ? held_bytes(sctx[s]) : 0.0;
+          bud.reserved += keep - res[s];
+          res[s] = keep;
         }
-        q_cv.notify_all();
+        bud.cv.notify_all();
       };
+      std::vector<hb_status> sctx_st(nsub, HB_OK);
+      for (int s = 0; s < nsub; ++s)  // cached stream contexts: their kept workspace counts from the start
+        sctx[s] = cached_context(devices[w], 1000 + slot[w] * 16 + s, &sctx_st[s]);
       std::vector<int64_t> first_q(nsub);  // stream 0 starts with the costliest problem
-      for (int s = 0; s < nsub; ++s) first_q[s] = take_ex(s >= nsub - nback, false);
+      for (int s = 0; s < nsub; ++s) first_q[s] = take_ex(s, s >= nsub - nback, false);
       std::vector<std::thread> sth;
       std::mutex sub_mu;
       std::vector<std::string> trace_lines;
       const double sweep_t0 = hb::host_now();
       auto sub_worker = [&](int s) {
-        hb_status ss = HB_OK;
-        hb_context* sc = cached_context(devices[w], 1000 + slot[w] * 16 + s, &ss);
+        const hb_status ss = sctx_st[s];
+        hb_context* sc = sctx[s];
         const bool from_back = s >= nsub - nback;
-        int64_t q0 = first_q[s] == -2 ? take(from_back) : first_q[s];
+        auto take = [&] { return take_ex(s, from_back, true); };
+        int64_t q0 = first_q[s] == -2 ? take() : first_q[s];
         if (!sc) {
-          for (int64_t q = q0; q >= 0; q = take(from_back)) {
+          for (int64_t q = q0; q >= 0; q = take()) {
             st[small[q]] = ss;
-            done_big(q);
+            finished(s, q);
           }
           return;
         }
@@ -698,7 +876,7 @@ hb_status hb_sweep_ex(const hb_problem* probs, int64_t n, const int32_t* devices
         sc->profiling = c->profiling;
         cudaStreamWaitEvent(sc->stream, ready, 0);
         static const bool timeline = getenv("HB_TIMELINE") != nullptr;
-        for (int64_t q = q0; q >= 0; q = take(from_back)) {
+        for (int64_t q = q0; q >= 0; q = take()) {
           const hb_problem& p = probs[small[q]];
           cudaEvent_t e0 = nullptr, e1 = nullptr;
           if (timeline) {
@@ -710,13 +888,14 @@ hb_status hb_sweep_ex(const hb_problem* probs, int64_t n, const int32_t* devices
           const hb::HostTrace h0 = hb::host_trace();
           const double t0 = ht ? hb::host_now() : 0.0;
           st[small[q]] = hb_rank(sc, &p.kernel, &p.pair, p.tols, p.ntol, out + offset[small[q]]);
-          if (is_big(small[q])) {  // give the pool back its big buffers before the cap opens
+          if (is_big(small[q]) || st[small[q]] == HB_ENOMEM) {
+            // give the pool back the big buffers before the next admission
             try {
               hb::context_trim(sc, kTrimBytes);
             } catch (const hb::Error&) {
             }
-            done_big(q);
           }
+          finished(s, q);
           if (ht) {
             const hb::HostTrace& h1 = hb::host_trace();
             char buf[256];
@@ -752,6 +931,12 @@ hb_status hb_sweep_ex(const hb_problem* probs, int64_t n, const int32_t* devices
       for (auto& l : trace_lines) fputs(l.c_str(), stderr);
       for (auto* sc : subs) cudaStreamWaitEvent(c->stream, sc->ev[5], 0);
       cudaEventDestroy(ready);
+      {  // this sweep's streams no longer reserve anything; what they keep is accounted when a
+         // later sweep's stream takes its first problem
+        std::lock_guard<std::mutex> lk(bud.mu);
+        for (int s = 0; s < nsub; ++s) bud.reserved -= res[s];
+      }
+      bud.cv.notify_all();
     }
     // device span of this worker: first event to last completion on its streams
     cudaEvent_t end;

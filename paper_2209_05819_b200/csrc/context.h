@@ -68,7 +68,14 @@ T* ws(hb_context* c, int id, size_t elems) {
   auto& b = c->bufs[id];
   const size_t bytes = std::max<size_t>(elems, 1) * sizeof(T);
   if (b.cap < bytes) {
-    if (b.p) HB_CUDA(cudaFreeAsync(b.p, c->stream));
+    if (b.p) {
+      void* old = b.p;
+      // forget the old buffer before anything can throw: a failed allocation below must not
+      // leave a freed pointer behind with its (larger) capacity for the next call to reuse
+      b.p = nullptr;
+      b.cap = 0;
+      HB_CUDA(cudaFreeAsync(old, c->stream));
+    }
     const size_t nb = bytes + bytes / 8;  // headroom
     HB_CUDA(cudaMallocAsync(&b.p, nb, c->stream));
     b.cap = nb;

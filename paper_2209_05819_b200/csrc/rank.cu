@@ -455,9 +455,11 @@ void rank_matrix_inplace(hb_context* c, double* A, int64_t m, int64_t n, int64_t
   int cert_kind[HB_MAX_TOLS] = {0, 0, 0, 0};
   SigmaAnswer ans[2 * HB_MAX_TOLS];
   int64_t k = 0;
-  int rounds = 0;
+  // certifications done and open-bracket predictor skips, counted apart so a skip never uses up
+  // one of the re-certification attempts (up to 4 certifications, up to 3 skips)
+  int certs = 0, skips = 0;
   double last_slope = 0.0;  // log-decay of |R_jj| per index near the threshold (0: unknown)
-  for (;; ++rounds) {
+  for (;;) {
     while (j < kmax) {
       const int b_req = (int)std::min<int64_t>({(int64_t)b, kmax - j, (int64_t)kBlockMax});
       const int64_t n_tr = n - j, mp = m - j;
@@ -610,7 +612,7 @@ void rank_matrix_inplace(hb_context* c, double* A, int64_t m, int64_t n, int64_t
     // pivoted QR); when more than 0.1 σ are expected, η drops to the value that expects 0.1
     // (>= η/5) before the first certification.  A wrong guess costs time only — the
     // certification below stays rigorous.
-    if (j < kmax && rounds < 3 && delta2 == INFINITY && sigma1_est > 0.0) {
+    if (j < kmax && skips < 3 && certs < 3 && delta2 == INFINITY && sigma1_est > 0.0) {
       static const bool predict = [] {
         const char* e = getenv("HB_PREDICT_OPEN");
         return !(e && atoi(e) == 0);
@@ -644,6 +646,7 @@ void rank_matrix_inplace(hb_context* c, double* A, int64_t m, int64_t n, int64_t
             const double eta_new = std::max(0.2 * eta_cur, std::sqrt(2.0 * 0.1 * slope));
             if (eta_new < 0.9 * eta_cur) {
               eta_cur = eta_new;
+              ++skips;
               continue;
             }
           }
@@ -707,7 +710,8 @@ void rank_matrix_inplace(hb_context* c, double* A, int64_t m, int64_t n, int64_t
       else if (nq > ntol && ans[ntol + t].rank_hi == ans[t].rank_lo) cert_kind[t] = 2;
       open |= cert_kind[t] == 0;
     }
-    if (!open || j >= kmax || rounds >= 3) break;
+    ++certs;
+    if (!open || j >= kmax || certs >= 4) break;
     // open bracket: with a density estimate, the η expecting ~0.02 σ in the window (in [η/5, η/2]);
     // without one, η/5
     eta_cur = last_slope > 0.0 ? std::min(0.5 * eta_cur, std::max(0.2 * eta_cur, std::sqrt(2.0 * 0.02 * last_slope)))

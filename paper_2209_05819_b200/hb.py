@@ -97,6 +97,15 @@ class hb_block(ctypes.Structure):
                 ("col_begin", ctypes.c_int64), ("cols", ctypes.c_int64)]
 
 
+class hb_interaction(ctypes.Structure):
+    """InteractionClass (geometry.hpp:77-104): kind SELF / SURFACE / FAR + d'."""
+    _fields_ = [("kind", ctypes.c_int32), ("surface_dim", ctypes.c_int32)]
+
+
+IC_SELF, IC_SURFACE, IC_FAR = 0, 1, 2
+DPRIME_FAR, DPRIME_SELF = -1, -2
+
+
 class hb_problem(ctypes.Structure):
     _fields_ = [("kernel", hb_kernel), ("pair", hb_pair), ("tols", ctypes.c_double * MAX_TOLS),
                 ("ntol", ctypes.c_int32), ("reserved", ctypes.c_int32)]
@@ -109,6 +118,7 @@ EXPORTS = [
     "hb_eval_radial_host", "hb_rank_matrix", "hb_rank", "hb_last_sigma", "hb_sweep",
     "hb_partition", "hb_problem_seed", "hb_rank_complex", "hb_phase_name", "hb_context_set_profiling",
     "hb_stats_get", "hb_stats_reset", "hb_sweep_ex", "hb_sweep_release", "hb_context_set_stopping",
+    "hb_classify_pair", "hb_classify_cubes", "hb_interaction_dprime", "hb_assemble_dense_host",
     # include/hb_debug.h (test hooks)
     "hb_debug_dgemm", "hb_debug_dgemm_async",
     # ACA (aca.hpp)
@@ -146,6 +156,16 @@ def load(path: os.PathLike | str | None = None):
     L.hb_generate_points.argtypes = [c_p, ctypes.POINTER(hb_pair), c_p, c_p]
     L.hb_assemble.argtypes = [c_p, ctypes.POINTER(hb_kernel), c_p, ctypes.c_int64, c_p,
                               ctypes.c_int64, ctypes.c_int32, c_p, ctypes.c_int64]
+    L.hb_classify_pair.argtypes = [ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(ctypes.c_int32),
+                                   ctypes.c_int32, ctypes.POINTER(ctypes.c_int32),
+                                   ctypes.POINTER(hb_interaction)]
+    L.hb_classify_cubes.argtypes = [ctypes.POINTER(hb_cube), ctypes.POINTER(hb_cube),
+                                    ctypes.POINTER(hb_interaction)]
+    L.hb_interaction_dprime.argtypes = [hb_interaction]
+    L.hb_interaction_dprime.restype = ctypes.c_int32
+    L.hb_assemble_dense_host.argtypes = [c_p, ctypes.POINTER(hb_kernel), c_p, ctypes.c_int64, c_p,
+                                         ctypes.c_int64, ctypes.c_int32, c_p, ctypes.c_int64,
+                                         ctypes.c_int64]
     L.hb_eval_radial_host.argtypes = [ctypes.POINTER(hb_kernel), ctypes.c_double,
                                       ctypes.POINTER(ctypes.c_double)]
     L.hb_rank_matrix.argtypes = [c_p, c_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
@@ -199,7 +219,8 @@ def load(path: os.PathLike | str | None = None):
                  "hb_assemble", "hb_eval_radial_host", "hb_rank_matrix", "hb_rank",
                  "hb_last_sigma", "hb_sweep", "hb_partition", "hb_context_set_profiling",
                  "hb_stats_get", "hb_stats_reset", "hb_sweep_ex", "hb_debug_dgemm",
-                 "hb_debug_dgemm_async"):
+                 "hb_debug_dgemm_async", "hb_classify_pair", "hb_classify_cubes",
+                 "hb_assemble_dense_host"):
         getattr(L, name).restype = ctypes.c_int
     if path is None:
         _lib = L
@@ -285,6 +306,26 @@ def eval_radial_host(kernel: hb_kernel, r: float) -> float:
     return out.value
 
 
+def classify_pair(level_a: int, grid_a: Sequence[int], level_b: int, grid_b: Sequence[int]):
+    """hodlr::classify_pair (geometry.hpp:109-118) -> (kind, d') with kind IC_SELF / IC_SURFACE /
+    IC_FAR.  Raises HBError(EINVAL) for different levels or dimensions, like the reference."""
+    if len(grid_a) != len(grid_b):
+        raise HBError(EINVAL, "classify_pair", "boxes have different dimensions")
+    d = len(grid_a)
+    ga = (ctypes.c_int32 * max(d, 1))(*grid_a)
+    gb = (ctypes.c_int32 * max(d, 1))(*grid_b)
+    out = hb_interaction()
+    _check(load().hb_classify_pair(d, level_a, ga, level_b, gb, ctypes.byref(out)), "hb_classify_pair")
+    return out.kind, out.surface_dim
+
+
+def classify_cubes(a: hb_cube, b: hb_cube):
+    out = hb_interaction()
+    _check(load().hb_classify_cubes(ctypes.byref(a), ctypes.byref(b), ctypes.byref(out)),
+           "hb_classify_cubes")
+    return out.kind, out.surface_dim
+
+
 @dataclass
 class RankResult:
     rank: int
@@ -346,6 +387,22 @@ class Context:
                  d_K: int, ldk: int):
         _check(self._lib.hb_assemble(self._h, ctypes.byref(kernel), d_tgt, T, d_src, N, d, d_K,
                                      ldk), "hb_assemble", self._h)
+
+    def assemble_dense_host(self, kernel: hb_kernel, targets, sources, entry_cap: int = 400_000_000):
+        """hodlr::assemble_dense (kernel.hpp:168-181) on host point sets: targets (d, T) and
+        sources (d, N) SoA float64 arrays (the PointSet layout) -> host K (T, N), Fortran order."""
+        import numpy as np
+        x = np.ascontiguousarray(targets, dtype=np.float64)
+        y = np.ascontiguousarray(sources, dtype=np.float64)
+        d, T = x.shape
+        d2, N = y.shape
+        if d != d2:
+            raise HBError(EINVAL, "assemble_dense", "point dimensions differ")
+        K = np.empty((T, N), dtype=np.float64, order="F")
+        _check(self._lib.hb_assemble_dense_host(self._h, ctypes.byref(kernel), x.ctypes.data, T,
+                                                y.ctypes.data, N, d, K.ctypes.data, T, entry_cap),
+               "hb_assemble_dense_host", self._h)
+        return K
 
     def rank(self, kernel: hb_kernel, pair: hb_pair, tols: Sequence[float]) -> list[RankResult]:
         nt = len(tols)
@@ -475,11 +532,13 @@ def sweep(problems: Sequence[hb_problem], devices: Sequence[int] = (0,), profili
     arr = (hb_problem * max(n, 1))(*problems)
     total = sum(p.ntol for p in problems)
     out = (hb_rank_result * max(total, 1))()
-    st = (ctypes.c_int32 * max(n, 1))()
+    st = (ctypes.c_int32 * max(n, 1))(*([-1] * max(n, 1)))  # -1: never written by the library
     devs = (ctypes.c_int32 * len(devices))(*devices)
     opts = hb_sweep_opts()
     opts.profiling = int(profiling)
-    load().hb_sweep_ex(arr, n, devs, len(devices), out, st, ctypes.byref(opts))
+    ret = load().hb_sweep_ex(arr, n, devs, len(devices), out, st, ctypes.byref(opts))
+    if n and any(v == -1 for v in st[:n]):  # an early failure (bad arguments) before any problem ran
+        _check(ret if ret != OK else EINVAL, "hb_sweep_ex")
     res, o = [], 0
     for p in problems:
         res.append([RankResult.of(out[o + t]) for t in range(p.ntol)])

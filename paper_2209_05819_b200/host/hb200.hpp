@@ -7,6 +7,9 @@
 //        <- hodlr::KernelId, KernelSpec, kernel_from_string, kernel_name, eval_radial
 //           (/root/reference/proj/include/hodlr/kernel.hpp:19-157)
 //   hb200::HyperCube, InteractionClass   <- hodlr::HyperCube, InteractionClass (geometry.hpp:15-104)
+//   hb200::BoxIndex, classify_pair       <- hodlr::BoxIndex, classify_pair (geometry.hpp:66-71, 106-118)
+//   hb200::assemble_dense                <- hodlr::assemble_dense (kernel.hpp:168-181), host
+//                                           PointSets in, host column-major Matrix out
 //   hb200::pair_geometry, epsilon_rank, rank_table, RankRecord, write_csv
 //        <- SPEC rankbench module (CSV schema SPEC.md:613)
 // Exceptions follow the reference: std::invalid_argument (HB_EINVAL), std::length_error
@@ -133,8 +136,20 @@ struct InteractionClass {  // geometry.hpp:77-104
   static InteractionClass self_block() { return {Kind::SelfBlock, -1}; }
   static InteractionClass shared_surface(int d_prime) { return {Kind::SharedSurface, d_prime}; }
   static InteractionClass far_field() { return {Kind::FarField, -1}; }
+  bool is_self() const { return kind == Kind::SelfBlock; }
   bool is_far() const { return kind == Kind::FarField; }
   bool is_vertex() const { return kind == Kind::SharedSurface && surface_dim == 0; }
+  bool shares_surface(int d_prime) const { return kind == Kind::SharedSurface && surface_dim == d_prime; }
+  friend bool operator==(const InteractionClass& a, const InteractionClass& b) {
+    return a.kind == b.kind && (a.kind != Kind::SharedSurface || a.surface_dim == b.surface_dim);
+  }
+  // hb_pair.d_prime encoding: HB_DPRIME_SELF (-2), HB_DPRIME_FAR (-1) or d'
+  int32_t dprime() const { return is_self() ? HB_DPRIME_SELF : (is_far() ? HB_DPRIME_FAR : surface_dim); }
+  static InteractionClass from_c(hb_interaction ic) {
+    if (ic.kind == HB_IC_SELF) return self_block();
+    if (ic.kind == HB_IC_FAR) return far_field();
+    return shared_surface(ic.surface_dim);
+  }
   std::string name() const {
     switch (kind) {
       case Kind::SelfBlock: return "self";
@@ -150,6 +165,30 @@ struct InteractionClass {  // geometry.hpp:77-104
     throw std::invalid_argument("unknown interaction: " + s);
   }
 };
+
+// BoxIndex (geometry.hpp:66-71): level + per-axis grid coordinate in [0, 2^level).
+struct BoxIndex {
+  int level = 0;
+  std::vector<int32_t> grid;
+  int dim() const { return static_cast<int>(grid.size()); }
+};
+
+// classify_pair (geometry.hpp:106-118): self / far (any offset >= 2) / surface:#zero offsets.
+inline InteractionClass classify_pair(const BoxIndex& a, const BoxIndex& b) {
+  if (a.grid.size() != b.grid.size())
+    throw std::invalid_argument("classify_pair: boxes have different dimensions");
+  hb_interaction ic{};
+  check(hb_classify_pair(a.dim(), a.level, a.grid.data(), b.level, b.grid.data(), &ic), "classify_pair");
+  return InteractionClass::from_c(ic);
+}
+
+// The same for two cubes of one uniform subdivision (equal sides, integer offsets).
+inline InteractionClass classify_pair(const HyperCube& a, const HyperCube& b) {
+  const hb_cube ca = a.to_c(), cb = b.to_c();
+  hb_interaction ic{};
+  check(hb_classify_cubes(&ca, &cb, &ic), "classify_pair");
+  return InteractionClass::from_c(ic);
+}
 
 enum class PointMode { Uniform = HB_POINTS_UNIFORM, GridInterior = HB_POINTS_GRID_INTERIOR,
                        GridClosed = HB_POINTS_GRID_CLOSED };
@@ -167,7 +206,7 @@ struct PairGeometry {
     hb_pair p{};
     p.target = target.to_c();
     p.source = source.to_c();
-    p.d_prime = interaction.is_far() ? -1 : interaction.surface_dim;
+    p.d_prime = interaction.dprime();
     p.point_mode = static_cast<int32_t>(mode);
     p.n_target = n;
     p.n_source = n;
@@ -199,7 +238,7 @@ inline PairGeometry pair_geometry(int d, InteractionClass inter, int64_t n,
 }
 
 inline uint64_t problem_seed(uint64_t base, int d, const InteractionClass& inter, int64_t n) {
-  return hb_problem_seed(base, d, inter.is_far() ? -1 : inter.surface_dim, n);
+  return hb_problem_seed(base, d, inter.dprime(), n);
 }
 
 // SPEC RankRecord + certification data.
@@ -227,6 +266,39 @@ class Device {
  private:
   hb_context* ctx_ = nullptr;
 };
+
+// PointSet (types.hpp:14-15): column-major, points are rows -> coordinate k of point i at k*n + i.
+struct PointSet {
+  int64_t n = 0;
+  int d = 0;
+  std::vector<double> soa;
+};
+
+// Matrix (types.hpp:11): column-major rows x cols.
+struct Matrix {
+  int64_t rows = 0, cols = 0;
+  std::vector<double> data;
+  double operator()(int64_t i, int64_t j) const { return data[(size_t)(j * rows + i)]; }
+};
+
+// assemble_dense (kernel.hpp:168-181): K(i, j) = F(‖targets_i − sources_j‖), assembled on the
+// device from host point sets, returned as a host column-major Matrix.  Same exceptions:
+// empty set / dimension mismatch -> invalid_argument, T·N > entry_cap -> length_error,
+// r == 0 on a singular kernel without a diagonal value -> runtime_error.
+inline Matrix assemble_dense(Device& dev, const KernelSpec& spec, const PointSet& targets,
+                             const PointSet& sources, int64_t entry_cap = 400'000'000) {
+  if (targets.n == 0 || sources.n == 0) throw std::invalid_argument("assemble_dense: empty point set");
+  if (targets.d != sources.d) throw std::invalid_argument("assemble_dense: point dimensions differ");
+  Matrix K;
+  K.rows = targets.n;
+  K.cols = sources.n;
+  K.data.resize((size_t)(targets.n * sources.n));
+  const hb_kernel ck = spec.to_c();
+  check(hb_assemble_dense_host(dev.get(), &ck, targets.soa.data(), targets.n, sources.soa.data(),
+                               sources.n, targets.d, K.data.data(), K.rows, entry_cap),
+        "assemble_dense", dev.get());
+  return K;
+}
 
 // SPEC epsilon_rank of one generated block: count of σ_k > eps·σ₁.
 inline std::vector<RankRecord> epsilon_rank(Device& dev, const KernelSpec& k, const PairGeometry& g,

@@ -114,3 +114,71 @@ def test_context_create_without_gpu_fails_loudly(hb):
         pytest.skip("GPU present")
     with pytest.raises(hb.HBError):
         hb.Context(0)
+
+
+# ---- classify_pair (geometry.hpp:109-118) ------------------------------------------------------
+
+def _golden_classify():
+    import json
+    from conftest import GOLDEN
+    return json.loads((GOLDEN / "classify_golden.json").read_text())
+
+
+def test_classify_pair_matches_reference_golden(hb):
+    """hb_classify_pair equals the reference's own classify_pair (compiled in oracle/_ref and
+    frozen by tests/golden/make_classify_golden.py) on every ordered box pair of the uniform
+    subdivisions d=1 level 3, d=2/3 level 2, d=4 level 1."""
+    g = _golden_classify()
+    n = 0
+    for case in g["cases"]:
+        d, level, grids = case["d"], case["level"], case["grids"]
+        nb = len(grids)
+        for a in range(nb):
+            for b in range(nb):
+                want = case["packed"][a * nb + b]
+                kind, sdim = hb.classify_pair(level, grids[a], level, grids[b])
+                assert (kind, sdim) == (want >> 4, (want & 15) - 1), (d, grids[a], grids[b])
+                n += 1
+    assert n == 4672
+    with pytest.raises(hb.HBError) as e:
+        hb.classify_pair(1, [0, 0], 2, [0, 0])
+    assert e.value.status == g["different_levels_status"] == hb.hb.EINVAL
+
+
+def test_classify_pair_matches_compiled_reference_live(hb, oracle):
+    """Same check against the live compiled reference (skipped where /root/reference is absent),
+    plus random grids at deeper levels."""
+    if not oracle.ref_available():
+        pytest.skip("oracle/_ref not built (no /root/reference)")
+    import random
+    L = oracle.ref_lib()
+    rng = random.Random(5)
+    for _ in range(3000):
+        d = rng.randint(1, 6)
+        level = rng.randint(0, 6)
+        ga = [rng.randrange(1 << level) for _ in range(d)]
+        gb = [min((1 << level) - 1, max(0, x + rng.randint(-2, 2))) for x in ga]
+        a = (ctypes.c_int32 * d)(*ga)
+        b = (ctypes.c_int32 * d)(*gb)
+        kind, sdim = ctypes.c_int32(), ctypes.c_int32()
+        assert L.hbr_classify_pair(d, level, a, level, b, ctypes.byref(kind), ctypes.byref(sdim)) == 0
+        assert hb.classify_pair(level, ga, level, gb) == (kind.value, sdim.value)
+
+
+def test_classify_cubes_and_pair_geometry(hb):
+    """The BASELINE pair geometry (source = target + o) classifies to the d' it
+    is built for; non-grid cube pairs are rejected like a different-level BoxIndex pair."""
+    for d in range(1, 5):
+        for dp in list(range(d)) + [None]:
+            p = hb.make_pair(d, dp, 10, hb.UNIFORM, 0)
+            kind, sdim = hb.classify_cubes(p.target, p.source)
+            if dp is None:
+                assert kind == hb.IC_FAR
+            else:
+                assert (kind, sdim) == (hb.IC_SURFACE, dp)
+    c = hb.make_cube([0.0, 0.0])
+    assert hb.classify_cubes(c, c) == (hb.IC_SELF, -1)
+    with pytest.raises(hb.HBError):
+        hb.classify_cubes(c, hb.make_cube([0.5, 0.0]))       # not on one grid
+    with pytest.raises(hb.HBError):
+        hb.classify_cubes(c, hb.make_cube([1.0, 0.0], 2.0))  # different sides

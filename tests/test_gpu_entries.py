@@ -177,3 +177,52 @@ def test_update_gemm_numerics(ctx, hb, M, N, K, ldpad):
     err = (C[:, :M].t() - ref).abs().max().item() / ref.abs().max().item()
     assert err < 1e-14 * max(1.0, K ** 0.5), err
     assert torch.equal(C[:, M:], keep)  # padding rows untouched
+
+
+def test_dprime_validated_against_cubes(ctx, hb):
+    """d_prime must equal classify_pair of the cube pair when the cubes are boxes of one grid
+    (geometry.hpp:109-118); a mismatch is an invalid_argument (EINVAL), not a silent relabel."""
+    for d, dp, wrong in [(2, 1, 0), (3, None, 2), (4, 0, -1), (1, 0, -2)]:
+        p = hb.make_pair(d, dp, 64, hb.UNIFORM, 0)
+        p.d_prime = wrong
+        with pytest.raises(hb.HBError) as e:
+            ctx.rank(hb.make_kernel("exp_neg_r"), p, [1e-12])
+        assert e.value.status == 1
+    p = hb.make_pair(2, 1, 64, hb.UNIFORM, 0)
+    p.d_prime = 5  # out of range for d = 2
+    with pytest.raises(hb.HBError):
+        ctx.rank(hb.make_kernel("exp_neg_r"), p, [1e-12])
+    # cubes off the common grid: d_prime cannot be implied and any valid label is accepted
+    p = hb.make_pair(2, 1, 64, hb.UNIFORM, 0)
+    p.source.lower[0] = 1.25
+    assert ctx.rank(hb.make_kernel("exp_neg_r"), p, [1e-12])[0].rank > 0
+
+
+@pytest.mark.parametrize("d,dp,T,N,kname", [(2, 1, 500, 700, "log_r"), (3, None, 64, 1000, "one_over_r"),
+                                            (4, 3, 333, 129, "exp_neg_r"), (1, 0, 1, 1, "sin_r")])
+def test_assemble_dense_host_matches_oracle(ctx, hb, oracle, d, dp, T, N, kname):
+    """hb_assemble_dense_host: the reference's assemble_dense(spec, targets, sources) on host
+    PointSets (kernel.hpp:168-181), same layout, entries within 1e-13 of the oracle (pinned bit
+    for bit against the compiled reference in tests/test_oracle.py)."""
+    x = oracle.points(d, [0.0] * d, 1.0, T, 0, 7, 0)
+    y = oracle.points(d, hb.offset(d, dp), 1.0, N, 0, 7, 1)
+    K = ctx.assemble_dense_host(hb.make_kernel(kname), x, y)
+    Ko = oracle.assemble(oracle.KERNEL_IDS[kname], x, y)
+    assert K.shape == (T, N)
+    np.testing.assert_allclose(K, Ko, rtol=TOL_REL, atol=0)
+
+
+def test_assemble_dense_host_errors(ctx, hb):
+    x = np.zeros((2, 10))
+    with pytest.raises(hb.HBError) as e:  # length_error: T*N above the entry cap (kernel.hpp:174-175)
+        ctx.assemble_dense_host(hb.make_kernel("log_r"), x, x + 1.0, entry_cap=50)
+    assert e.value.status == 3
+    with pytest.raises(hb.HBError) as e:  # empty point set (kernel.hpp:171)
+        ctx.assemble_dense_host(hb.make_kernel("log_r"), np.zeros((2, 0)), x)
+    assert e.value.status == 1
+    with pytest.raises(hb.HBError) as e:  # point dimensions differ (kernel.hpp:172-173)
+        ctx.assemble_dense_host(hb.make_kernel("log_r"), np.zeros((3, 4)), x)
+    assert e.value.status == 1
+    with pytest.raises(hb.HBError) as e:  # r == 0 on 1/r without a diagonal (kernel.hpp:152-153)
+        ctx.assemble_dense_host(hb.make_kernel("one_over_r", diagonal=None), x, x)
+    assert e.value.status == 4

@@ -289,3 +289,31 @@ def test_rectangular_complex_pair(ctx, hb, oracle):
     B = oracle.assemble(oracle.KERNEL_IDS["helmholtz3d_im"], x, y)
     s = oracle.singular_values(A + 1j * B)
     assert r.rank == oracle.epsilon_rank_from_sigma(s, 1e-12).rank and r.rank_lo == r.rank_hi
+
+
+def test_sweep_two_workers_one_device_matches_single(ctx, hb):
+    """hb_sweep_ex with devices = [0, 0]: two in-process workers (LPT split over the two entries,
+    one shared device-memory budget) give exactly the single-worker results, problem by problem —
+    the in-process analogue of parallel_for over independent blocks (parallel.hpp:12-29)."""
+    spec = [(1, 0, "log_r", 1000), (2, None, "exp_neg_r", 2000), (3, 1, "one_over_r", 1000),
+            (4, 2, "exp_neg_r", 1000), (2, 1, "log_r", 4000), (3, None, "log_r", 3000),
+            (4, 3, "one_over_r", 2000), (1, None, "exp_neg_r", 8000), (2, 0, "one_over_r", 20000)]
+    probs = [hb.make_problem(k, d, dp, n, [1e-12, 1e-10]) for (d, dp, k, n) in spec]
+    one, st1 = hb.sweep(probs, [0])
+    two, st2 = hb.sweep(probs, [0, 0])
+    assert st1 == st2 == [0] * len(probs)
+    own = hb.partition(probs, 2)
+    assert set(own) == {0, 1}
+    for a, b in zip(one, two):
+        assert [x.rank for x in a] == [x.rank for x in b]
+        assert [x.k_factored for x in a] == [x.k_factored for x in b]
+        assert [x.sigma1 for x in a] == [x.sigma1 for x in b]
+
+
+def test_sweep_bad_arguments_raise(hb):
+    """An early hb_sweep_ex failure (ntol out of range) is reported, not read back as rank 0."""
+    p = hb.make_problem("log_r", 1, 0, 100, [1e-12])
+    p.ntol = 0
+    with pytest.raises(hb.HBError) as e:
+        hb.sweep([p], [0])
+    assert e.value.status == 1

@@ -195,3 +195,37 @@ def test_golden_baseline_fixture_consistent(oracle, baseline_ranks):
                                   seed=r["seed"], nthreads=nthreads())
         assert [g.rank for g in got] == r["ranks"]
         assert r["seed"] == oracle.problem_seed(0, r["d"], r["dprime"], r["N"])
+
+
+# ---- certified large-N route (oracle/certified.py) ---------------------------------------------
+
+@pytest.mark.parametrize("d,dp,kname,n", [(2, 1, "log_r", 1000), (3, 2, "one_over_r", 1000),
+                                          (4, 3, "exp_neg_r", 1000), (4, None, "one_over_r", 1500),
+                                          (1, 0, "exp_neg_r", 800)])
+def test_certified_route_equals_full_svd(oracle, d, dp, kname, n):
+    """dgeqp3rk + dgesdd(R_k) + Weyl bracket (the oracle's route for N >= 16000) reproduces the
+    full-SVD ε-rank and certifies it (rank_lo == rank_hi) — SPEC.md:560-568."""
+    from oracle import certified as C
+    tols = [1e-12, 1e-10]
+    seed = oracle.problem_seed(0, d, dp, n)
+    x, y = oracle.pair_points(d, dp, n, oracle.UNIFORM, seed)
+    K = oracle.assemble(oracle.KERNEL_IDS[kname], x, y, nthreads=nthreads())
+    full = [oracle.epsilon_rank_from_sigma(oracle.singular_values(K), t).rank for t in tols]
+    c = C.certified_rank(K.copy(order="F"), tols)
+    assert c.rank_lo == c.rank_hi == c.ranks == full
+    assert c.k >= max(full) and c.delta_F <= 0.25 * min(tols) * c.sigma1 * 1.0001
+
+
+def test_golden_large_n_records_are_certified(baseline_ranks):
+    """Every large-N golden record (certified route) closed its bracket; the N = 8000 records it
+    was validated on (tests/golden/certified_validation.json) equal the full-SVD ranks."""
+    import json
+    from conftest import GOLDEN
+    cert = [r for r in baseline_ranks if r.get("oracle", "").startswith("certified")]
+    for r in cert:
+        assert r["rank_lo"] == r["rank_hi"] == r["ranks"], r
+        assert r["k"] >= max(r["ranks"])
+    vp = GOLDEN / "certified_validation.json"
+    if vp.exists():
+        for v in json.loads(vp.read_text()):
+            assert v["equal"] and v["ranks"] == v["full_svd_ranks"], v
