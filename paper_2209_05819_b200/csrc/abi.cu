@@ -1064,3 +1064,30 @@ extern "C" hb_status hb_debug_dgemm(hb_context* ctx, int32_t transA, int64_t M, 
   if (s != HB_OK) return s;
   return guarded(ctx, [&] { HB_CUDA(cudaStreamSynchronize(ctx->stream)); });
 }
+
+extern "C" hb_status hb_debug_dgemm_fro(hb_context* ctx, int32_t transA, int64_t M, int64_t N, int64_t K,
+                                        double alpha, const double* A, int64_t lda, const double* B,
+                                        int64_t ldb, double beta, double* C, int64_t ldc, int64_t fro_row0,
+                                        double* fro_out) {
+  if (!ctx || !fro_out) return HB_EINVAL;
+  return guarded(ctx, [&] {
+    if (M < 0 || N < 0 || K < 0) throw Error(HB_EINVAL, "negative size");
+    HB_CUDA(cudaSetDevice(ctx->device));
+    const int64_t cnt = hb::gemm_fro_count(M, N, K, ctx->num_sms);
+    double* parts = hb::ws<double>(ctx, hb::B_FRO, (size_t)cnt);
+    double* sum = hb::ws<double>(ctx, hb::B_FROSUM, 8);
+    hb::GemmArgs g{};
+    g.M = M; g.N = N; g.K = K; g.alpha = alpha; g.A = A; g.lda = lda; g.transA = transA != 0;
+    g.B = B; g.ldb = ldb; g.beta = beta; g.C = C; g.ldc = ldc;
+    g.fro_partials = parts;
+    g.fro_row0 = fro_row0;
+    const int64_t wse = 8ll << 20;
+    double* sk = hb::ws<double>(ctx, hb::B_SPLITK, wse);
+    hb::launch_dgemm(g, sk, wse, ctx->num_sms, ctx->stream);
+    hb::sum_kernel<<<1, 1024, 0, ctx->stream>>>(parts, cnt, sum);
+    HB_LAUNCH_CHECK();
+    HB_CUDA(cudaMemcpyAsync(fro_out, sum, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    HB_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+

@@ -20,6 +20,11 @@
 #include "common.cuh"
 #include "kernels.h"
 
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
 namespace hb {
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
@@ -393,12 +398,101 @@ static int choose_slices(int64_t M, int64_t N, int64_t K, int num_sms, int64_t w
   return best;
 }
 
-int64_t gemm_fro_count(int64_t M, int64_t N, int64_t K) {
-  return std::max<int64_t>(tiles_of(M, N, K), kReduceBlocks);
+// TMA-fed persistent-strip kernel for the NN shapes (dgemm_tma.cu)
+bool tma_gemm_eligible(const GemmArgs& g);
+int64_t tma_gemm_fro_count(int64_t M, int64_t N, int num_sms);
+void launch_dgemm_tma(const GemmArgs& g, int num_sms, cudaStream_t st);
+
+// Frobenius partial slots a GEMM of this shape may write (either kernel); unused ones are zeroed.
+int64_t gemm_fro_count(int64_t M, int64_t N, int64_t K, int num_sms) {
+  const int64_t a = std::max<int64_t>(tiles_of(M, N, K), (int64_t)kReduceBlocks);
+  return std::max<int64_t>(a, tma_gemm_fro_count(M, N, num_sms));
+}
+
+// HB_GEMM_CHECK=1 (diagnostics): every TMA-routed GEMM is re-run by the cp.async kernel on a copy
+// of C and the two results (and Frobenius sums) are compared on the host.
+__global__ void gemm_check_diff(const double* C, int64_t ldc, const double* D, int64_t M, int64_t N,
+                                double* out) {
+  double mx = 0.0, ref = 0.0;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < M * N;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t m = idx % M, n = idx / M;
+    const double a = C[m + n * ldc], b = D[idx];
+    mx = fmax(mx, fabs(a - b));
+    ref = fmax(ref, fabs(b));
+  }
+  atomicMax(reinterpret_cast<unsigned long long*>(out), __double_as_longlong(mx));
+  atomicMax(reinterpret_cast<unsigned long long*>(out + 1), __double_as_longlong(ref));
+}
+
+void launch_dgemm(const GemmArgs& g, double* ws, int64_t ws_elems, int num_sms, cudaStream_t st);
+
+static void checked_tma(const GemmArgs& g, double* ws, int64_t ws_elems, int num_sms, cudaStream_t st) {
+  double *D = nullptr, *F = nullptr, *out = nullptr;
+  const int64_t cnt = gemm_fro_count(g.M, g.N, g.K, num_sms);
+  HB_CUDA(cudaMallocAsync(&D, sizeof(double) * g.M * g.N, st));
+  HB_CUDA(cudaMallocAsync(&F, sizeof(double) * (cnt + 2), st));
+  HB_CUDA(cudaMallocAsync(&out, sizeof(double) * 4, st));
+  HB_CUDA(cudaMemsetAsync(out, 0, sizeof(double) * 4, st));
+  HB_CUDA(cudaMemcpy2DAsync(D, g.M * 8, g.C, g.ldc * 8, g.M * 8, g.N, cudaMemcpyDeviceToDevice, st));
+  GemmArgs r = g;
+  r.C = D;
+  r.ldc = g.M;
+  r.fro_partials = g.fro_partials ? F : nullptr;
+  launch_dgemm_tma(g, num_sms, st);
+  setenv("HB_GEMM_TMA_FORCE_OFF", "1", 1);
+  launch_dgemm(r, ws, ws_elems, num_sms, st);
+  unsetenv("HB_GEMM_TMA_FORCE_OFF");
+  gemm_check_diff<<<296, 256, 0, st>>>(g.C, g.ldc, D, g.M, g.N, out);
+  std::vector<double> hp(cnt), hq(cnt);
+  double h[2];
+  HB_CUDA(cudaMemcpyAsync(h, out, sizeof(h), cudaMemcpyDeviceToHost, st));
+  if (g.fro_partials) {
+    const int64_t written = tma_gemm_fro_count(g.M, g.N, num_sms);
+    HB_CUDA(cudaMemcpyAsync(hp.data(), g.fro_partials, sizeof(double) * written, cudaMemcpyDeviceToHost, st));
+    HB_CUDA(cudaMemcpyAsync(hq.data(), F, sizeof(double) * cnt, cudaMemcpyDeviceToHost, st));
+    HB_CUDA(cudaStreamSynchronize(st));
+    double a = 0, b = 0;
+    for (int64_t i = 0; i < written; ++i) a += hp[(size_t)i];
+    for (int64_t i = 0; i < cnt; ++i) b += hq[(size_t)i];
+    if (!(std::fabs(a - b) <= 1e-12 * std::fabs(b)))
+      fprintf(stderr, "[gemm check] FRO M=%lld N=%lld K=%lld: tma %.17g ref %.17g\n", (long long)g.M,
+              (long long)g.N, (long long)g.K, a, b);
+  }
+  HB_CUDA(cudaStreamSynchronize(st));
+  if (!(h[0] <= 1e-13 * h[1]))
+    fprintf(stderr, "[gemm check] C M=%lld N=%lld K=%lld lda=%lld ldb=%lld ldc=%lld A=%p B=%p C=%p: maxdiff %.3g ref %.3g\n",
+            (long long)g.M, (long long)g.N, (long long)g.K, (long long)g.lda, (long long)g.ldb,
+            (long long)g.ldc, (const void*)g.A, (const void*)g.B, (void*)g.C, h[0], h[1]);
+  // the caller's C must hold the TMA result (already there); the check buffers go back
+  HB_CUDA(cudaFreeAsync(D, st));
+  HB_CUDA(cudaFreeAsync(F, st));
+  HB_CUDA(cudaFreeAsync(out, st));
 }
 
 void launch_dgemm(const GemmArgs& g, double* ws, int64_t ws_elems, int num_sms, cudaStream_t st) {
   if (g.M <= 0 || g.N <= 0) return;
+  static const bool check = getenv("HB_GEMM_CHECK") != nullptr;
+  if (tma_gemm_eligible(g) && !getenv("HB_GEMM_TMA_FORCE_OFF")) {
+    if (check) {
+      checked_tma(g, ws, ws_elems, num_sms, st);
+      if (g.fro_partials) {
+        const int64_t written = tma_gemm_fro_count(g.M, g.N, num_sms);
+        const int64_t cnt = gemm_fro_count(g.M, g.N, g.K, num_sms);
+        if (cnt > written)
+          HB_CUDA(cudaMemsetAsync(g.fro_partials + written, 0, (cnt - written) * sizeof(double), st));
+      }
+      return;
+    }
+    launch_dgemm_tma(g, num_sms, st);
+    if (g.fro_partials) {
+      const int64_t written = tma_gemm_fro_count(g.M, g.N, num_sms);
+      const int64_t cnt = gemm_fro_count(g.M, g.N, g.K, num_sms);
+      if (cnt > written)
+        HB_CUDA(cudaMemsetAsync(g.fro_partials + written, 0, (cnt - written) * sizeof(double), st));
+    }
+    return;
+  }
   GemmParams p{};
   p.M = g.M; p.N = g.N; p.K = g.K;
   p.alpha = g.alpha; p.beta = g.beta;
@@ -441,14 +535,14 @@ void launch_dgemm(const GemmArgs& g, double* ws, int64_t ws_elems, int num_sms, 
     p.partial = ws;
     splitk_reduce<<<kReduceBlocks, 256, 0, st>>>(p, s_eff);
     HB_LAUNCH_CHECK();
-    const int64_t cnt = gemm_fro_count(g.M, g.N, g.K);
+    const int64_t cnt = gemm_fro_count(g.M, g.N, g.K, num_sms);
     if (g.fro_partials && cnt > kReduceBlocks)
       HB_CUDA(cudaMemsetAsync(g.fro_partials + kReduceBlocks, 0, (cnt - kReduceBlocks) * sizeof(double), st));
   } else if (g.fro_partials) {
     // pad the partial array to the fixed count with zeros so the consumer can always sum
     // gemm_fro_count(M, N) entries
     const int64_t written = tiles_of(g.M, g.N, g.K);
-    const int64_t cnt = gemm_fro_count(g.M, g.N, g.K);
+    const int64_t cnt = gemm_fro_count(g.M, g.N, g.K, num_sms);
     if (cnt > written)
       HB_CUDA(cudaMemsetAsync(g.fro_partials + written, 0, (cnt - written) * sizeof(double), st));
   }

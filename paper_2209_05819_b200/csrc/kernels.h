@@ -39,7 +39,7 @@ struct GemmArgs {
 };
 void launch_dgemm(const GemmArgs& g, double* splitk_ws, int64_t splitk_ws_elems, int num_sms,
                   cudaStream_t st);
-int64_t gemm_fro_count(int64_t M, int64_t N, int64_t K);  // partials written for this shape
+int64_t gemm_fro_count(int64_t M, int64_t N, int64_t K, int num_sms);  // partial slots for this shape
 
 // ---- sketch ----------------------------------------------------------------------------------
 void launch_gaussian(double* omega, int64_t rows, int64_t cols, int64_t ld, uint64_t seed,

@@ -190,24 +190,27 @@ void panel_and_T(hb_context* c, double* P, int64_t ld, int64_t mp, int b, double
 void apply_block_reflector(hb_context* c, const double* V, int64_t ldv, const double* T, int b,
                            double* A2, int64_t ld, int64_t mp, int64_t n2, double* fro_dev) {
   if (n2 <= 0) return;
-  double* W = ws<double>(c, B_W, (size_t)kBlockMax * n2);
-  double* W2 = ws<double>(c, B_W2, (size_t)kBlockMax * n2);
+  // W, W2 with an even leading dimension (multiple of 8): 16-byte column strides keep the update
+  // GEMM on the TMA-fed kernel for any block width b
+  const int64_t ldw = round_up(b, 8);
+  double* W = ws<double>(c, B_W, (size_t)ldw * n2);
+  double* W2 = ws<double>(c, B_W2, (size_t)ldw * n2);
   Gemm gemm{c};
   GemmArgs g{};
   g.M = b; g.N = n2; g.K = mp; g.alpha = 1.0; g.A = V; g.lda = ldv; g.transA = true;
-  g.B = A2; g.ldb = ld; g.beta = 0.0; g.C = W; g.ldc = b;
+  g.B = A2; g.ldb = ld; g.beta = 0.0; g.C = W; g.ldc = ldw;
   gemm(g);
   GemmArgs g2{};
   g2.M = b; g2.N = n2; g2.K = b; g2.alpha = 1.0; g2.A = T; g2.lda = b; g2.transA = true;
-  g2.B = W; g2.ldb = b; g2.beta = 0.0; g2.C = W2; g2.ldc = b;
+  g2.B = W; g2.ldb = ldw; g2.beta = 0.0; g2.C = W2; g2.ldc = ldw;
   gemm(g2);
   GemmArgs g3{};
   g3.M = mp; g3.N = n2; g3.K = b; g3.alpha = -1.0; g3.A = V; g3.lda = ldv; g3.transA = false;
-  g3.B = W2; g3.ldb = b; g3.beta = 1.0; g3.C = A2; g3.ldc = ld;
+  g3.B = W2; g3.ldb = ldw; g3.beta = 1.0; g3.C = A2; g3.ldc = ld;
   double* parts = nullptr;
   int64_t cnt = 0;
   if (fro_dev) {
-    cnt = gemm_fro_count(mp, n2, b);
+    cnt = gemm_fro_count(mp, n2, b, c->num_sms);
     parts = ws<double>(c, B_FRO, (size_t)cnt);
     g3.fro_partials = parts;
     g3.fro_row0 = b;

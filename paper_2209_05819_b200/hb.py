@@ -120,7 +120,7 @@ EXPORTS = [
     "hb_stats_get", "hb_stats_reset", "hb_sweep_ex", "hb_sweep_release", "hb_context_set_stopping",
     "hb_classify_pair", "hb_classify_cubes", "hb_interaction_dprime", "hb_assemble_dense_host",
     # include/hb_debug.h (test hooks)
-    "hb_debug_dgemm", "hb_debug_dgemm_async",
+    "hb_debug_dgemm", "hb_debug_dgemm_async", "hb_debug_dgemm_fro",
     # ACA (aca.hpp)
     "hb_aca_compress", "hb_aca_factor_info", "hb_aca_factor_copy", "hb_aca_apply",
     "hb_aca_factor_destroy",
@@ -202,6 +202,8 @@ def load(path: os.PathLike | str | None = None):
           c_p, ctypes.c_int64, c_p, ctypes.c_int64, ctypes.c_double, c_p, ctypes.c_int64]
     L.hb_debug_dgemm.argtypes = dg
     L.hb_debug_dgemm_async.argtypes = dg + [ctypes.c_int32]
+    L.hb_debug_dgemm_fro.argtypes = dg + [ctypes.c_int64, ctypes.POINTER(ctypes.c_double)]
+    L.hb_debug_dgemm_fro.restype = ctypes.c_int
     L.hb_aca_compress.argtypes = [c_p, ctypes.POINTER(hb_kernel), c_p, ctypes.c_int64, c_p,
                                   ctypes.c_int64, ctypes.c_int32, ctypes.POINTER(hb_block),
                                   ctypes.c_int64, ctypes.c_double, ctypes.c_int64,
@@ -450,6 +452,16 @@ class Context:
         else:
             _check(self._lib.hb_debug_dgemm(self._h, int(transA), M, N, K, alpha, A, lda, B, ldb,
                                             beta, C, ldc), "dgemm", self._h)
+
+    def dgemm_fro(self, transA: bool, M: int, N: int, K: int, alpha: float, A: int, lda: int,
+                  B: int, ldb: int, beta: float, C: int, ldc: int, fro_row0: int) -> float:
+        """Test hook: the GEMM with the trailing update's Frobenius epilogue; returns the sum of
+        squares of the new C over rows >= fro_row0."""
+        out = ctypes.c_double()
+        _check(self._lib.hb_debug_dgemm_fro(self._h, int(transA), M, N, K, alpha, A, lda, B, ldb,
+                                            beta, C, ldc, fro_row0, ctypes.byref(out)),
+               "dgemm_fro", self._h)
+        return out.value
 
     def aca_compress(self, kernel: hb_kernel, d_tgt: int, nt: int, d_src: int, ns: int, d: int,
                      blocks, eps: float, max_rank: int) -> list["ACAFactor"]:

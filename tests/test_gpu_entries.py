@@ -157,6 +157,31 @@ def test_dgemm_hook_numerics(ctx, hb):
         assert err < 1e-14 * max(1.0, K ** 0.5), (ta, M, N, K, err)
 
 
+@pytest.mark.parametrize("M,N,K,offs", [(20000, 19880, 120, (1, 0, 0)), (4000, 3000, 120, (0, 1, 0)),
+                                        (4000, 3000, 117, (1, 1, 1)), (3001, 2999, 128, (1, 0, 1)),
+                                        (513, 777, 100, (0, 1, 1)), (256, 256, 96, (1, 1, 0)),
+                                        (1000, 300, 121, (0, 0, 1))])
+def test_update_gemm_pointer_offsets(ctx, hb, M, N, K, offs):
+    """Operands starting 8 bytes past a 16-byte boundary (odd column offsets inside K, V and W
+    buffers): the TMA-fed kernel loads from the aligned boundary and reads at +1."""
+    g = torch.Generator(device="cuda").manual_seed(M + K)
+    oa, ob, oc = offs
+    ld, ldb = M + 8, K + 8
+    A = torch.randn(ld * K + 8, dtype=torch.float64, device="cuda", generator=g)
+    B = torch.randn(ldb * N + 8, dtype=torch.float64, device="cuda", generator=g)
+    C = torch.randn(ld * N + 8, dtype=torch.float64, device="cuda", generator=g)
+    Am = A[oa:oa + ld * K].view(K, ld).t()[:M]
+    Bm = B[ob:ob + ldb * N].view(N, ldb).t()[:K]
+    Cm = C[oc:oc + ld * N].view(N, ld).t()[:M]
+    ref = Cm - Am @ Bm
+    torch.cuda.synchronize()
+    ctx.dgemm(False, M, N, K, -1.0, A.data_ptr() + 8 * oa, ld, B.data_ptr() + 8 * ob, ldb, 1.0,
+              C.data_ptr() + 8 * oc, ld)
+    torch.cuda.synchronize()
+    err = (Cm - ref).abs().max().item() / ref.abs().max().item()
+    assert err < 1e-14 * max(1.0, K ** 0.5), err
+
+
 @pytest.mark.parametrize("M,N,K,ldpad", [(5000, 333, 120, 0), (1000, 1000, 64, 0), (777, 4097, 117, 3),
                                          (4096, 257, 8, 1), (300, 300, 1, 0), (2048, 2048, 128, 0),
                                          (16001, 1500, 97, 5), (4000, 4000, 120, 0),
