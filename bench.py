@@ -403,6 +403,10 @@ def main():
                                  "gpu": r.rank, "oracle": g["ranks"][t], "gap_oracle": g["gaps"][t],
                                  "gap_gpu": r.gap})
     uncert = sum(1 for res in full for r in res if r.certificate == 0)
+    # exact-arithmetic brackets whose σ sit within the QR's rounding band of the threshold
+    in_band = [{"problem": list(wl[j % len(wl)][:4]), "tol": wl[j % len(wl)][4][t], "gap": r.gap,
+                "fp_band": r.fp_band} for j, res in enumerate(full) for t, r in enumerate(res)
+               if r.gap < r.fp_band]
     prob_cert = sum(1 for res in full for r in res if r.certificate == 2)
     path_tf = total_alg * args.steps / t_dev / 1e12
     line = {
@@ -428,6 +432,8 @@ def main():
         "clocks": clocks,
         "parity": {"checked_vs_oracle": checked, "equal": equal, "mismatches": mism[:20],
                    "uncertified_brackets": uncert, "probabilistic_certificates": prob_cert,
+                   "rounding_sensitive": {"count": len(in_band), "cases": in_band[:10],
+                                          "rule": "gap < fp_band = sqrt(N) u ||A||_F / thr"},
                    "statuses_ok": all(s == 0 for s in statuses),
                    "failed": [[list(w[:4]), s] for w, s in zip([wl[i % len(wl)] for i in mine], statuses) if s != 0][:10],
                    "last_error": hb.load().hb_last_error(None).decode()[:200]},

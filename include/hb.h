@@ -24,6 +24,7 @@
  *   hb_rank_complex        <- the paper's complex F3 / F4 tables from the
  *                             reference's real/imaginary kernel pairs (kernel.hpp:22-27)
  *   hb_sweep               <- SPEC rank_table + parallel_for        SPEC.md:570-578, parallel.hpp:12-29
+ *   hb_fit_growth          <- SPEC fit_growth (rank vs {1, log N, N^c}) SPEC.md:580-588
  *   hb_block               <- hodlr::BlockSpec index ranges         aca.hpp:16-28
  *   hb_aca_factor          <- hodlr::ACAFactor                      aca.hpp:50-62
  *   hb_aca_compress        <- hodlr::compress (aca_sweep)           aca.hpp:72-198
@@ -118,8 +119,12 @@ typedef struct {
   double sec[4];       /* device seconds: points+assembly, factorisation, certification, total */
   int32_t certificate; /* 1: rank_lo == rank_hi with δ = ‖A22‖_F (deterministic bound);
                           2: rank_lo == rank_hi with δ = 2·(power-method estimate of ‖A22‖₂),
-                             valid with probability >= 1 - 1e-27; 0: bracket open */
+                             valid with probability >= 1 - 1e-27; 0: bracket open.
+                          The bracket is exact-arithmetic: see fp_band for rounding. */
   int32_t reserved;
+  double fp_band;      /* sqrt(N)·u·‖A‖_F / thr: the relative size of the Householder QR's backward
+                          error at the threshold.  gap < fp_band flags a count that rounding could
+                          move (reported, like a boundary tie) */
 } hb_rank_result;
 
 #define HB_MAX_TOLS 4
@@ -217,6 +222,24 @@ hb_status hb_last_sigma(hb_context* ctx, double* host_out, int64_t max, int64_t*
  * go to status_out (may be NULL); the return value is the first failure or HB_OK. */
 hb_status hb_sweep(const hb_problem* probs, int64_t n, const int32_t* devices, int32_t ndev,
                    hb_rank_result* out, int32_t* status_out);
+
+/* SPEC fit_growth: least-squares fits of rank(N) for one kernel / interaction
+ * series by the three growth laws of the paper's theorems — constant (far field), a + b·log N
+ * (vertex, Theorem 1), a·N^c (d'-surface, Theorem 2: c = d'/d) — each with its residual sum of
+ * squares; `best` is the model with the lowest BIC, n·ln(RSS/n + s²) + params·ln n with
+ * s = 1e-3·mean(rank) (so exact fits tie towards the simpler law).  Fewer than 4 distinct N ->
+ * HB_EINVAL (the fit is refused), as are non-positive N or negative ranks. */
+enum { HB_GROWTH_CONSTANT = 0, HB_GROWTH_LOG = 1, HB_GROWTH_POWER = 2 };
+typedef struct {
+  int32_t best;          /* HB_GROWTH_* */
+  int32_t n;             /* points used */
+  double constant;       /* constant model: rank = constant */
+  double log_a, log_b;   /* log model: rank = log_a + log_b * ln N */
+  double pow_a, pow_c;   /* power model: rank = pow_a * N^pow_c */
+  double rss[3];         /* residual sum of squares per model */
+  double max_min_ratio;  /* max rank / min rank of the series */
+} hb_growth_fit;
+hb_status hb_fit_growth(const int64_t* N, const double* rank, int32_t n, hb_growth_fit* out);
 
 /* ---- profiling: per-phase device time from CUDA events on the context stream (off by
  * default; the events add ~µs per phase) and the process-wide kernel-launch counter ---------- */

@@ -11,5 +11,5 @@ from .hb import (  # noqa: F401
     hb_rank_result, load, make_cube, make_kernel, make_pair, make_problem, offset, partition,
     problem_seed, sweep, global_stats, reset_global_stats, sweep_release, hb_stats, PHASES,
     ACAFactor, hb_block, classify_pair, classify_cubes, hb_interaction, hb_cube, IC_SELF,
-    IC_SURFACE, IC_FAR, DPRIME_FAR, DPRIME_SELF,
+    IC_SURFACE, IC_FAR, DPRIME_FAR, DPRIME_SELF, fit_growth,
 )

@@ -464,6 +464,88 @@ hb_status hb_classify_cubes(const hb_cube* a, const hb_cube* b, hb_interaction* 
 
 int32_t hb_interaction_dprime(hb_interaction ic) { return dprime_of(ic); }
 
+hb_status hb_fit_growth(const int64_t* N, const double* rank, int32_t n, hb_growth_fit* out) {
+  return guarded(nullptr, [&] {
+    if (!N || !rank || !out) throw Error(HB_EINVAL, "fit_growth: NULL argument");
+    std::vector<double> x, y;
+    for (int32_t i = 0; i < n; ++i) {
+      if (N[i] <= 0 || !(rank[i] >= 0.0)) throw Error(HB_EINVAL, "fit_growth: N must be > 0, rank >= 0");
+      x.push_back((double)N[i]);
+      y.push_back(rank[i]);
+    }
+    std::vector<double> xs(x);
+    std::sort(xs.begin(), xs.end());
+    if (std::unique(xs.begin(), xs.end()) - xs.begin() < 4)
+      throw Error(HB_EINVAL, "fit_growth: fewer than 4 distinct N values");
+    const double m = (double)x.size();
+    double ym = 0.0, ymin = INFINITY, ymax = 0.0;
+    for (double v : y) { ym += v; ymin = std::min(ymin, v); ymax = std::max(ymax, v); }
+    ym /= m;
+    hb_growth_fit f{};
+    f.n = (int32_t)x.size();
+    f.max_min_ratio = ymin > 0.0 ? ymax / ymin : INFINITY;
+    // constant
+    f.constant = ym;
+    for (double v : y) f.rss[0] += (v - ym) * (v - ym);
+    // a + b ln N (ordinary least squares)
+    auto linfit = [&](const std::vector<double>& u, double* a, double* b) {
+      double um = 0.0;
+      for (double v : u) um += v;
+      um /= m;
+      double sxy = 0.0, sxx = 0.0;
+      for (size_t i = 0; i < u.size(); ++i) {
+        sxy += (u[i] - um) * (y[i] - ym);
+        sxx += (u[i] - um) * (u[i] - um);
+      }
+      *b = sxx > 0.0 ? sxy / sxx : 0.0;
+      *a = ym - *b * um;
+    };
+    std::vector<double> lx(x.size());
+    for (size_t i = 0; i < x.size(); ++i) lx[i] = std::log(x[i]);
+    linfit(lx, &f.log_a, &f.log_b);
+    for (size_t i = 0; i < x.size(); ++i) {
+      const double r = y[i] - (f.log_a + f.log_b * lx[i]);
+      f.rss[1] += r * r;
+    }
+    // a N^c: for fixed c the best a is closed-form; c by golden-section search on [0, 2]
+    auto rss_pow = [&](double c, double* a_out) {
+      double num = 0.0, den = 0.0;
+      for (size_t i = 0; i < x.size(); ++i) {
+        const double t = std::pow(x[i], c);
+        num += t * y[i];
+        den += t * t;
+      }
+      const double a = den > 0.0 ? num / den : 0.0;
+      double r2 = 0.0;
+      for (size_t i = 0; i < x.size(); ++i) {
+        const double r = y[i] - a * std::pow(x[i], c);
+        r2 += r * r;
+      }
+      if (a_out) *a_out = a;
+      return r2;
+    };
+    double lo = 0.0, hi = 2.0;
+    const double gr = 0.5 * (std::sqrt(5.0) - 1.0);
+    double c1 = hi - gr * (hi - lo), c2 = lo + gr * (hi - lo);
+    double f1 = rss_pow(c1, nullptr), f2 = rss_pow(c2, nullptr);
+    for (int it = 0; it < 200 && hi - lo > 1e-12; ++it) {
+      if (f1 <= f2) { hi = c2; c2 = c1; f2 = f1; c1 = hi - gr * (hi - lo); f1 = rss_pow(c1, nullptr); }
+      else { lo = c1; c1 = c2; f1 = f2; c2 = lo + gr * (hi - lo); f2 = rss_pow(c2, nullptr); }
+    }
+    f.pow_c = 0.5 * (lo + hi);
+    f.rss[2] = rss_pow(f.pow_c, &f.pow_a);
+    // model choice: BIC with a floor on the residual scale (ties go to fewer parameters)
+    const double s2 = (1e-3 * ym) * (1e-3 * ym) + 1e-300;
+    const int params[3] = {1, 2, 2};
+    double best = INFINITY;
+    for (int k = 0; k < 3; ++k) {
+      const double bic = m * std::log(f.rss[k] / m + s2) + params[k] * std::log(m);
+      if (bic < best - 1e-9) { best = bic; f.best = k; }
+    }
+    *out = f;
+  });
+}
+
 hb_status hb_assemble_dense_host(hb_context* ctx, const hb_kernel* kernel, const double* tgt, int64_t T,
                                  const double* src, int64_t N, int32_t d, double* K, int64_t ldk,
                                  int64_t entry_cap) {

@@ -901,6 +901,21 @@ __global__ void iota_kernel(int64_t* __restrict__ p, int64_t n) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i < n) p[i] = i;
 }
+// Sum of squares of a column-major m x n matrix: block b sums a fixed grid-strided subset into
+// parts[b] (fixed order, deterministic); sum_kernel folds the partials.
+__global__ void sumsq_kernel(const double* __restrict__ A, int64_t m, int64_t n, int64_t ld,
+                             double* __restrict__ parts) {
+  __shared__ double red[32];
+  double s = 0.0;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < m * n;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const double v = A[idx % m + (idx / m) * ld];
+    s += v * v;
+  }
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) parts[blockIdx.x] = s;
+}
+
 __global__ void nonfinite_kernel(const double* __restrict__ A, int64_t m, int64_t n, int64_t ld,
                                  unsigned int* flags) {
   const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;

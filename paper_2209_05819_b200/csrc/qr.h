@@ -63,20 +63,6 @@ struct PowerParams {
   GridBarrier bar;
 };
 
-struct BidiagParams {
-  double* M;  // k x k, column-major (destroyed)
-  int64_t ld;
-  int64_t k;
-  double* d;      // [k]   diagonal of the upper bidiagonal
-  double* e;      // [k]   superdiagonal (k-1 used)
-  double* wslot;  // [G][k] column partials
-  double* w;      // [k]
-  double* v;      // [k]
-  double* nslot;  // [G]
-  double* scal;   // [4] broadcast scalars
-  GridBarrier bar;
-};
-
 __global__ void sketch_cpqr_kernel(SketchParams p);
 // Shared-memory-resident variant (sketch columns of a CTA fit in ~200 KB): one barrier per pivot,
 // the winner's column travels through a per-CTA candidate slot instead of the global sketch.
@@ -92,11 +78,11 @@ __global__ void sketch_trsm_kernel(const double* Y1, int64_t ldy, int ell, const
                                    int64_t ldr, int b, double* Z, int64_t ldz);
 __global__ void power_sigma1_kernel(PowerParams p);
 __global__ void sum_kernel(const double* parts, int64_t n, double* out);
+__global__ void sumsq_kernel(const double* A, int64_t m, int64_t n, int64_t ld, double* parts);
 __global__ void gram_sigma1_kernel(const double* G, int b, int iters, double* out);
 __global__ void transpose_upper_kernel(const double* A, int64_t lda, int64_t k, int64_t n, double* B,
                                        int64_t ldb);
 __global__ void copy_upper_kernel(const double* B, int64_t ldb, int64_t k, double* C, int64_t ldc);
-__global__ void bidiag_kernel(BidiagParams p);
 
 // Bisection on the upper bidiagonal (d, e): singular-value queries.
 struct SigmaQuery {

@@ -424,6 +424,13 @@ void rank_matrix_inplace(hb_context* c, double* A, int64_t m, int64_t n, int64_t
   iota_kernel<<<(unsigned)ceil_div(std::max<int64_t>(n, 1), 256), 256, 0, c->stream>>>(perm, n);
   HB_LAUNCH_CHECK();
 
+  {  // ‖A‖_F² -> scal[2], for the rounding band of the certificate (read with the first block)
+    double* parts = ws<double>(c, B_FRO, 592);
+    sumsq_kernel<<<592, 256, 0, st>>>(A, m, n, lda, parts);
+    sum_kernel<<<1, 1024, 0, st>>>(parts, 592, scal + 2);
+    HB_LAUNCH_CHECK();
+  }
+  double fro_a2 = -1.0;
   uint64_t sketch_seed = 0x243F6A8885A308D3ull;
   if (kmax > 0) {
     Phase ph(c, HB_PH_SKETCH);
@@ -542,9 +549,10 @@ void rank_matrix_inplace(hb_context* c, double* A, int64_t m, int64_t n, int64_t
         Gemm{c}(g);
       }
       j += bh;
-      double hs[2];
+      double hs[3];
       sync_to_host(c, scal, hs, sizeof(hs));
       delta = std::sqrt(std::max(hs[0], 0.0));
+      if (fro_a2 < 0.0) fro_a2 = hs[2];
       if (first) {
         sigma1_est = hs[1];
         first = false;
@@ -754,6 +762,15 @@ void rank_matrix_inplace(hb_context* c, double* A, int64_t m, int64_t n, int64_t
     }
     r.gap = gap;
     r.certificate = cert_kind[t];
+    // Householder QR is backward stable: the computed factors are exact for A + E with
+    // ‖E‖ ≈ sqrt(N)·u·‖A‖_F; relative to the threshold that is the band a count could move by
+    if (fro_a2 < 0.0) {  // no block ran (tiny problem): read ‖A‖_F² now
+      double h3[3];
+      sync_to_host(c, scal, h3, sizeof(h3));
+      fro_a2 = h3[2];
+    }
+    r.fp_band = thr > 0.0 ? std::sqrt((double)std::max(m, n)) * 0x1p-53 * std::sqrt(std::max(fro_a2, 0.0)) / thr
+                          : 0.0;
     r.resid = cert_kind[t] == 2 ? delta2 : delta;
     if (cert_kind[t] == 2) r.rank_hi = ans[ntol + t].rank_hi;
     r.sec[1] = f_ms * 1e-3;

@@ -5,163 +5,11 @@
 // test count(σ > tol·σ₁) and the boundary gap only need σ₁, σ_p, σ_{p+1} and two counts, which
 // bisection on the bidiagonal delivers to high relative accuracy without computing the rest.
 //
-// bidiag_kernel (grid-cooperative): rows are dealt to CTAs in 32-row blocks, block-cyclically;
-// a warp processes one column segment of 32 rows at a time (coalesced 256-byte accesses).  Per
-// step i: left reflector u from column i (partial norms -> barrier), wᵀ = uᵀM (partials ->
-// barrier -> distributed reduce -> barrier), rank-1 update, right reflector v from row i (owner
-// CTA -> barrier), z = M v and rank-1 update done row-locally (no reduction across CTAs).
 #include "common.cuh"
 #include "kernels.h"
 #include "qr.h"
 
 namespace hb {
-
-__global__ void __launch_bounds__(256) bidiag_kernel(BidiagParams p) {
-  GridSync gbar(p.bar);
-  extern __shared__ double bsm[];
-  const int G = gridDim.x, g = blockIdx.x;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t k = p.k, ld = p.ld;
-  double* M = p.M;
-  const int64_t nb = ceil_div(k, 32);
-  const int64_t nown = g < nb ? ceil_div(nb - g, G) : 0;  // own blocks: g, g+G, ...
-  double* u = bsm;                      // [nown*32]
-  double* zp = bsm + nown * 32;         // [8][nown*32]
-  __shared__ double sh[4];
-  __shared__ double red[32];
-
-  auto own_row = [&](int64_t t) { return (g + t * G) * 32; };
-
-  // partial norm of column 0 (rows > 0)
-  {
-    double s = 0.0;
-    if (warp == 0)
-      for (int64_t t = 0; t < nown; ++t) {
-        const int64_t r = own_row(t) + lane;
-        if (r > 0 && r < k) { const double x = M[r]; s += x * x; }
-      }
-    s = warp_sum(s);
-    if (tid == 0) p.nslot[g] = s;
-  }
-  gbar.sync();
-
-  for (int64_t i = 0; i < k; ++i) {
-    // ---- left reflector from column i ----
-    const double s_all = block_sum_strided(p.nslot, G, 1, red);
-    if (tid == 0) {
-      const double s = s_all;
-      const double alpha = M[i + i * ld];
-      double tau = 0.0, scal = 0.0, beta = alpha;
-      if (s > 0.0) {
-        beta = -copysign(sqrt(alpha * alpha + s), alpha);
-        tau = (beta - alpha) / beta;
-        scal = 1.0 / (alpha - beta);
-      }
-      sh[0] = tau; sh[1] = scal;
-      if (g == 0) p.d[i] = beta;
-    }
-    __syncthreads();
-    const double tau_u = sh[0], scal_u = sh[1];
-    for (int64_t e = tid; e < nown * 32; e += 256) {
-      const int64_t r = own_row(e / 32) + (e % 32);
-      double ur = 0.0;
-      if (r < k) ur = r > i ? M[r + i * ld] * scal_u : (r == i ? 1.0 : 0.0);
-      u[e] = ur;
-    }
-    __syncthreads();
-    const int64_t t0 = i / 32 >= g ? (i / 32 - g + G - 1) / G : 0;  // first own block with rows >= i
-    if (i + 1 < k) {
-      for (int64_t q = i + 1 + warp; q < k; q += 8) {
-        const double* col = M + q * ld;
-        double s = 0.0;
-        for (int64_t t = t0; t < nown; ++t) {
-          const int64_t r = own_row(t) + lane;
-          if (r >= i && r < k) s += u[t * 32 + lane] * col[r];
-        }
-        s = warp_sum(s);
-        if (lane == 0) p.wslot[(size_t)g * k + q] = s;
-      }
-    }
-    gbar.sync();
-    if (i + 1 < k) {
-      for (int64_t q = i + 1 + g + (int64_t)warp * G; q < k; q += (int64_t)G * 8) {
-        const double s = warp_sum_strided(p.wslot + q, G, k);
-        if (lane == 0) p.w[q] = s * tau_u;
-      }
-    }
-    gbar.sync();
-    if (i + 1 >= k) break;
-    // ---- apply left reflector: M[r, q] -= u_r w_q ----
-    for (int64_t q = i + 1 + warp; q < k; q += 8) {
-      double* col = M + q * ld;
-      const double wq = p.w[q];
-      for (int64_t t = t0; t < nown; ++t) {
-        const int64_t r = own_row(t) + lane;
-        if (r >= i && r < k) col[r] -= u[t * 32 + lane] * wq;
-      }
-    }
-    __syncthreads();
-    // ---- right reflector from row i (owner CTA) ----
-    const bool owner = ((i / 32) % G) == g;
-    if (owner) {
-      if (warp == 0) {
-        double s = 0.0;
-        for (int64_t q = i + 2 + lane; q < k; q += 32) { const double x = M[i + q * ld]; s += x * x; }
-        s = warp_sum(s);
-        const double alpha = M[i + (i + 1) * ld];
-        double tau = 0.0, scal = 0.0, beta = alpha;
-        if (s > 0.0) {
-          beta = -copysign(sqrt(alpha * alpha + s), alpha);
-          tau = (beta - alpha) / beta;
-          scal = 1.0 / (alpha - beta);
-        }
-        for (int64_t q = i + 2 + lane; q < k; q += 32) p.v[q] = M[i + q * ld] * scal;
-        if (lane == 0) {
-          p.v[i + 1] = 1.0;
-          p.scal[0] = tau;
-          p.e[i] = beta;
-        }
-      }
-    }
-    gbar.sync();
-    const double tau_v = p.scal[0];
-    // ---- z = M v for own rows r > i, then M[r, q] -= z_r v_q ----
-    for (int64_t e = tid; e < 8 * nown * 32; e += 256) zp[e] = 0.0;
-    __syncthreads();
-    for (int64_t q = i + 1 + warp; q < k; q += 8) {
-      const double* col = M + q * ld;
-      const double vq = p.v[q];
-      for (int64_t t = t0; t < nown; ++t) {
-        const int64_t r = own_row(t) + lane;
-        if (r > i && r < k) zp[warp * nown * 32 + t * 32 + lane] += col[r] * vq;
-      }
-    }
-    __syncthreads();
-    for (int64_t e = tid; e < nown * 32; e += 256) {
-      double s = 0.0;
-      for (int w = 0; w < 8; ++w) s += zp[w * nown * 32 + e];
-      u[e] = s * tau_v;  // reuse u as z
-    }
-    __syncthreads();
-    double nrm = 0.0;
-    for (int64_t q = i + 1 + warp; q < k; q += 8) {
-      double* col = M + q * ld;
-      const double vq = p.v[q];
-      for (int64_t t = t0; t < nown; ++t) {
-        const int64_t r = own_row(t) + lane;
-        if (r > i && r < k) {
-          const double x = col[r] - u[t * 32 + lane] * vq;
-          col[r] = x;
-          if (q == i + 1 && r > i + 1) nrm += x * x;
-        }
-      }
-    }
-    // partial norm of column i+1 (rows > i+1): owned by the warp with q == i+1 (warp 0)
-    nrm = warp_sum(nrm);
-    if (tid == 0) p.nslot[g] = nrm;
-    gbar.sync();
-  }
-}
 
 // ---- bisection on the TGK matrix of the upper bidiagonal (d, e) ----------------------------
 // count_less(x) = #singular values < x (x > 0): Sturm count of TGK − xI over the off-diagonal

@@ -10,19 +10,19 @@ from typing import Callable, Sequence
 
 from .hb import RankResult, hb_problem, partition
 
-REC = 16  # float64 fields per packed record
+REC = 17  # float64 fields per packed record
 
 
 def pack(idx: int, t: int, r: RankResult) -> list[float]:
     return [float(idx), float(t), float(r.rank), float(r.rank_lo), float(r.rank_hi),
             float(r.k_factored), r.sigma1, r.sigma_r, r.sigma_r1, r.gap, r.resid] + list(r.sec) + \
-        [float(r.certificate)]
+        [float(r.certificate), r.fp_band]
 
 
 def unpack(row) -> tuple[int, int, RankResult]:
     v = [float(x) for x in row]
     return int(v[0]), int(v[1]), RankResult(int(v[2]), int(v[3]), int(v[4]), int(v[5]), v[6], v[7],
-                                            v[8], v[9], v[10], v[11:15], int(v[15]))
+                                            v[8], v[9], v[10], v[11:15], int(v[15]), v[16])
 
 
 def my_share(problems: Sequence[hb_problem], rank: int, world: int) -> list[int]:

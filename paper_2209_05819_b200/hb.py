@@ -62,7 +62,7 @@ class hb_rank_result(ctypes.Structure):
                 ("sigma_r", ctypes.c_double), ("sigma_r1", ctypes.c_double),
                 ("gap", ctypes.c_double), ("resid", ctypes.c_double),
                 ("sec", ctypes.c_double * 4), ("certificate", ctypes.c_int32),
-                ("reserved", ctypes.c_int32)]
+                ("reserved", ctypes.c_int32), ("fp_band", ctypes.c_double)]
 
     def as_dict(self) -> dict:
         return {f: (list(getattr(self, f)) if f == "sec" else getattr(self, f))
@@ -106,6 +106,17 @@ IC_SELF, IC_SURFACE, IC_FAR = 0, 1, 2
 DPRIME_FAR, DPRIME_SELF = -1, -2
 
 
+class hb_growth_fit(ctypes.Structure):
+    """SPEC fit_growth result."""
+    _fields_ = [("best", ctypes.c_int32), ("n", ctypes.c_int32), ("constant", ctypes.c_double),
+                ("log_a", ctypes.c_double), ("log_b", ctypes.c_double), ("pow_a", ctypes.c_double),
+                ("pow_c", ctypes.c_double), ("rss", ctypes.c_double * 3),
+                ("max_min_ratio", ctypes.c_double)]
+
+
+GROWTH_MODELS = ["constant", "log", "power"]
+
+
 class hb_problem(ctypes.Structure):
     _fields_ = [("kernel", hb_kernel), ("pair", hb_pair), ("tols", ctypes.c_double * MAX_TOLS),
                 ("ntol", ctypes.c_int32), ("reserved", ctypes.c_int32)]
@@ -119,6 +130,7 @@ EXPORTS = [
     "hb_partition", "hb_problem_seed", "hb_rank_complex", "hb_phase_name", "hb_context_set_profiling",
     "hb_stats_get", "hb_stats_reset", "hb_sweep_ex", "hb_sweep_release", "hb_context_set_stopping",
     "hb_classify_pair", "hb_classify_cubes", "hb_interaction_dprime", "hb_assemble_dense_host",
+    "hb_fit_growth",
     # include/hb_debug.h (test hooks)
     "hb_debug_dgemm", "hb_debug_dgemm_async", "hb_debug_dgemm_fro",
     # ACA (aca.hpp)
@@ -161,6 +173,9 @@ def load(path: os.PathLike | str | None = None):
                                    ctypes.POINTER(hb_interaction)]
     L.hb_classify_cubes.argtypes = [ctypes.POINTER(hb_cube), ctypes.POINTER(hb_cube),
                                     ctypes.POINTER(hb_interaction)]
+    L.hb_fit_growth.argtypes = [ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_double),
+                                ctypes.c_int32, ctypes.POINTER(hb_growth_fit)]
+    L.hb_fit_growth.restype = ctypes.c_int
     L.hb_interaction_dprime.argtypes = [hb_interaction]
     L.hb_interaction_dprime.restype = ctypes.c_int32
     L.hb_assemble_dense_host.argtypes = [c_p, ctypes.POINTER(hb_kernel), c_p, ctypes.c_int64, c_p,
@@ -321,6 +336,18 @@ def classify_pair(level_a: int, grid_a: Sequence[int], level_b: int, grid_b: Seq
     return out.kind, out.surface_dim
 
 
+def fit_growth(ns: Sequence[int], ranks: Sequence[float]) -> dict:
+    """SPEC fit_growth through hb_fit_growth: constant / a + b ln N / a N^c."""
+    n = len(ns)
+    cn = (ctypes.c_int64 * max(n, 1))(*[int(v) for v in ns])
+    cr = (ctypes.c_double * max(n, 1))(*[float(v) for v in ranks])
+    out = hb_growth_fit()
+    _check(load().hb_fit_growth(cn, cr, n, ctypes.byref(out)), "hb_fit_growth")
+    return {"best": GROWTH_MODELS[out.best], "n": out.n, "constant": out.constant,
+            "log": (out.log_a, out.log_b), "power": (out.pow_a, out.pow_c),
+            "rss": dict(zip(GROWTH_MODELS, list(out.rss))), "max_min_ratio": out.max_min_ratio}
+
+
 def classify_cubes(a: hb_cube, b: hb_cube):
     out = hb_interaction()
     _check(load().hb_classify_cubes(ctypes.byref(a), ctypes.byref(b), ctypes.byref(out)),
@@ -341,11 +368,16 @@ class RankResult:
     resid: float
     sec: list
     certificate: int = 0  # 1 deterministic bracket, 2 probabilistic (<1e-27), 0 open
+    fp_band: float = 0.0  # sqrt(N)·u·‖A‖_F / thr; gap < fp_band: rounding-sensitive count
 
     @classmethod
     def of(cls, r: hb_rank_result) -> "RankResult":
         return cls(r.rank, r.rank_lo, r.rank_hi, r.k_factored, r.sigma1, r.sigma_r, r.sigma_r1,
-                   r.gap, r.resid, list(r.sec), r.certificate)
+                   r.gap, r.resid, list(r.sec), r.certificate, r.fp_band)
+
+    @property
+    def in_fp_band(self) -> bool:
+        return self.gap < self.fp_band
 
 
 class Context:

@@ -252,6 +252,7 @@ struct RankRecord {
   int rank_lo = 0, rank_hi = 0, k_factored = 0;
   double sigma1 = 0.0, sigma_r = 0.0, sigma_r1 = 0.0, gap = 0.0;
   double seconds = 0.0;
+  double fp_band = 0.0;  // sqrt(N)·u·‖A‖_F / thr: gap < fp_band means rounding could move the count
 };
 
 // RAII device context (one per device and host thread).
@@ -316,6 +317,7 @@ inline std::vector<RankRecord> epsilon_rank(Device& dev, const KernelSpec& k, co
     r.epsilon = eps[t]; r.rank = out[t].rank; r.rank_lo = out[t].rank_lo; r.rank_hi = out[t].rank_hi;
     r.k_factored = out[t].k_factored; r.sigma1 = out[t].sigma1; r.sigma_r = out[t].sigma_r;
     r.sigma_r1 = out[t].sigma_r1; r.gap = out[t].gap; r.seconds = out[t].sec[3];
+    r.fp_band = out[t].fp_band;
     recs.push_back(r);
   }
   return recs;
@@ -350,6 +352,29 @@ inline int epsilon_rank(Device& dev, const double* d_matrix, int64_t m, int64_t 
   hb_rank_result r{};
   check(hb_rank_matrix(dev.get(), d_matrix, m, n, ld, &eps, 1, &r), "epsilon_rank", dev.get());
   return r.rank;
+}
+
+// SPEC fit_growth: rank(N) against constant / a + b ln N / a N^c.
+struct GrowthFit {
+  std::string best;  // "constant" | "log" | "power"
+  double constant = 0, log_a = 0, log_b = 0, pow_a = 0, pow_c = 0, rss[3] = {0, 0, 0}, max_min_ratio = 0;
+};
+inline GrowthFit fit_growth(const std::vector<RankRecord>& recs) {
+  std::vector<int64_t> ns;
+  std::vector<double> rk;
+  for (const auto& r : recs) {
+    ns.push_back(r.N);
+    rk.push_back((double)r.rank);
+  }
+  hb_growth_fit f{};
+  check(hb_fit_growth(ns.data(), rk.data(), (int32_t)ns.size(), &f), "fit_growth");
+  static const char* names[3] = {"constant", "log", "power"};
+  GrowthFit g;
+  g.best = names[f.best];
+  g.constant = f.constant; g.log_a = f.log_a; g.log_b = f.log_b; g.pow_a = f.pow_a; g.pow_c = f.pow_c;
+  for (int k = 0; k < 3; ++k) g.rss[k] = f.rss[k];
+  g.max_min_ratio = f.max_min_ratio;
+  return g;
 }
 
 // SPEC rank_table: one record per (kernel, N), problems spread over the

@@ -2,7 +2,10 @@
 //
 //   rank-bench --d D --interaction far|surface:K --kernel NAME[,NAME...] --N n1[,n2...]
 //              [--epsilon 1e-12] [--grid uniform|interior|closed] [--seed S] [--devices 0[,1..]]
-//              [--out file.csv]
+//              [--out file.csv] [--fit 1]
+//
+// --fit 1: after the CSV, SPEC fit_growth of every kernel's rank(N) series with
+// at least 4 distinct N, one "# fit ..." line per kernel on stderr.
 //
 // NAME is a catalog kernel (kernel.hpp:112-129) or one of the paper's complex columns
 // "helmholtz3d" (F3 = e^{ir}/r) and "hankel_h12" (F4 = H_2^(1)(r)), ranked as K_re + i·K_im.
@@ -27,7 +30,7 @@ int usage(const char* msg) {
   std::fprintf(stderr,
                "rank-bench: %s\nusage: rank-bench --d D --interaction far|surface:K --kernel NAME[,..] "
                "--N n1[,..] [--epsilon E] [--grid uniform|interior|closed] [--seed S] "
-               "[--devices 0,..] [--out FILE]\n",
+               "[--devices 0,..] [--out FILE] [--fit 1]\n",
                msg);
   return 64;
 }
@@ -122,6 +125,21 @@ int main(int argc, char** argv) {
         std::fprintf(stderr, "error %s N=%lld: %s\n", recs[i].kernel.c_str(), (long long)recs[i].N,
                      hb_status_string(st[i]));
         rc = 1;
+      }
+    }
+    if (a.count("fit") && a["fit"] != "0") {
+      std::map<std::string, std::vector<hb200::RankRecord>> by;
+      for (size_t i = 0; i < recs.size(); ++i)
+        if (st[i] == HB_OK) by[recs[i].kernel].push_back(recs[i]);
+      for (const auto& [name, series] : by) {
+        try {
+          const auto g = hb200::fit_growth(series);
+          std::fprintf(stderr, "# fit %s: best %s, constant %.3f, log %.3f + %.3f ln N, power %.4g N^%.4f, "
+                       "rss %.4g/%.4g/%.4g, max/min %.3f\n", name.c_str(), g.best.c_str(), g.constant,
+                       g.log_a, g.log_b, g.pow_a, g.pow_c, g.rss[0], g.rss[1], g.rss[2], g.max_min_ratio);
+        } catch (const std::invalid_argument& e) {
+          std::fprintf(stderr, "# fit %s: refused (%s)\n", name.c_str(), e.what());
+        }
       }
     }
     hb_sweep_release();

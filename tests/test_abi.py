@@ -182,3 +182,36 @@ def test_classify_cubes_and_pair_geometry(hb):
         hb.classify_cubes(c, hb.make_cube([0.5, 0.0]))       # not on one grid
     with pytest.raises(hb.HBError):
         hb.classify_cubes(c, hb.make_cube([1.0, 0.0], 2.0))  # different sides
+
+
+# ---- fit_growth on the paper's own tables ------------------------------------
+
+def _series(paper_tables, label, kernel):
+    tab = next(t for t in paper_tables if t["label"] == label)
+    ci = tab["kernels"].index(kernel)
+    return [r["N"] for r in tab["rows"]], [r["ranks"][ci] for r in tab["rows"]]
+
+
+def test_fit_growth_spec_examples(hb, paper_tables):
+    """SPEC.md:585-588 / acceptance 2: far field constant (max/min <= 1.3), vertex best fit log with
+    a power exponent < 0.2, 2-D edge exponent 0.5 +- 0.1, 3-D face 0.667 +- 0.1 — on the paper's
+    published table values as fixtures."""
+    f = hb.fit_growth(*_series(paper_tables, "tab:res_2d_far", "one_over_r"))
+    assert f["best"] == "constant" and f["max_min_ratio"] <= 1.3
+    for label in ("tab:res_2d_ver", "tab:res_1d_vert", "tab:res_3d_ver"):
+        f = hb.fit_growth(*_series(paper_tables, label, "one_over_r"))
+        assert f["best"] == "log" and f["rss"]["log"] < f["rss"]["power"] and f["power"][1] < 0.2
+    f = hb.fit_growth(*_series(paper_tables, "tab:res_2d_edge", "log_r"))
+    assert f["best"] == "power" and abs(f["power"][1] - 0.5) <= 0.1
+    f = hb.fit_growth(*_series(paper_tables, "tab:res_3d_face", "one_over_r"))
+    assert f["best"] == "power" and abs(f["power"][1] - 2.0 / 3.0) <= 0.1
+
+
+def test_fit_growth_refuses_short_series(hb):
+    with pytest.raises(hb.HBError) as e:  # SPEC.md:584: fewer than 4 points -> fit refused
+        hb.fit_growth([1000, 2000, 4000, 4000], [5, 6, 7, 7])
+    assert e.value.status == 1
+    with pytest.raises(hb.HBError):
+        hb.fit_growth([1000, 0, 4000, 8000], [5, 6, 7, 8])
+    f = hb.fit_growth([1000, 2000, 4000, 8000], [10.0, 20.0, 40.0, 80.0])  # exact N^1
+    assert f["best"] == "power" and f["power"][1] == pytest.approx(1.0, abs=1e-6)

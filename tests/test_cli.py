@@ -42,3 +42,16 @@ def test_cli_paper_values(args, want):
     lines = r.stdout.strip().splitlines()
     assert lines[0].startswith("kernel,d,interaction,dprime,N,epsilon,rank,seconds")
     assert int(lines[1].split(",")[6]) == want
+
+
+@pytest.mark.gpu
+def test_cli_fit_growth():
+    """--fit 1: SPEC fit_growth on the computed series (2-D edge, log r, interior grids): the
+    power law wins with exponent near d'/d = 1/2."""
+    r = run("--d", "2", "--interaction", "surface:1", "--kernel", "log_r", "--N",
+            "1600,3600,6400,10000,14400", "--grid", "interior", "--fit", "1")
+    assert r.returncode == 0, r.stderr
+    line = next(ln for ln in r.stderr.splitlines() if ln.startswith("# fit log_r"))
+    assert "best power" in line
+    c = float(line.split("N^")[1].split(",")[0])
+    assert abs(c - 0.5) <= 0.15, line

@@ -327,3 +327,18 @@ def test_sweep_bad_arguments_reported(hb):
     p.ntol = 0
     _, st = hb.sweep([q, p], [0])
     assert st == [1, 1]
+
+
+def test_fp_band_reported(ctx, hb, oracle):
+    """Every result carries the rounding band of its exact-arithmetic certificate,
+    fp_band = sqrt(N)·u·‖A‖_F / (tol·σ₁), with ‖A‖_F from the device matches the oracle's entries."""
+    import numpy as np
+    d, dp, kname, n = 3, 1, "one_over_r", 1500
+    seed = hb.problem_seed(0, d, dp, n)
+    res = ctx.rank(hb.make_kernel(kname), hb.make_pair(d, dp, n, hb.UNIFORM, seed), [1e-12, 1e-8])
+    x, y = oracle.pair_points(d, dp, n, oracle.UNIFORM, seed)
+    fro = float(np.linalg.norm(oracle.assemble(oracle.KERNEL_IDS[kname], x, y)))
+    for r, tol in zip(res, [1e-12, 1e-8]):
+        want = np.sqrt(n) * 2.0 ** -53 * fro / (tol * r.sigma1)
+        assert r.fp_band == pytest.approx(want, rel=1e-9)
+        assert r.in_fp_band == (r.gap < r.fp_band)
