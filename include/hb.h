@@ -25,6 +25,10 @@
  *                             reference's real/imaginary kernel pairs (kernel.hpp:22-27)
  *   hb_sweep               <- SPEC rank_table + parallel_for        SPEC.md:570-578, parallel.hpp:12-29
  *   hb_fit_growth          <- SPEC fit_growth (rank vs {1, log N, N^c}) SPEC.md:580-588
+ *   hb_chebyshev_nodes     <- hodlr::chebyshev_nodes                chebyshev.hpp:16-23
+ *   hb_interpolation_decay <- hodlr::interpolation_decay            chebyshev.hpp:151-177
+ *   hb_fit_decay_rate      <- hodlr::fit_decay_rate                 chebyshev.hpp:180-193
+ *   hb_v_d_constant        <- hodlr::v_d_constant                   chebyshev.hpp:139-147
  *   hb_block               <- hodlr::BlockSpec index ranges         aca.hpp:16-28
  *   hb_aca_factor          <- hodlr::ACAFactor                      aca.hpp:50-62
  *   hb_aca_compress        <- hodlr::compress (aca_sweep)           aca.hpp:72-198
@@ -240,6 +244,23 @@ typedef struct {
   double max_min_ratio;  /* max rank / min rank of the series */
 } hb_growth_fit;
 hb_status hb_fit_growth(const int64_t* N, const double* rank, int32_t n, hb_growth_fit* out);
+
+/* ---- Chebyshev interpolation bound check (chebyshev.hpp:125-193) --------------------------------
+ * cos(pi k / p), k = 0..p (p + 1 values; p = 0 -> {0}); p < 0 -> HB_EINVAL. */
+hb_status hb_chebyshev_nodes(int32_t p, double* out);
+/* interpolation_decay: for each degree p_list[i], err_out[i] = max |K(X, S) - U V| over the
+ * reference's sample grid S of the cube (m^d interior points, m = 20 reduced until m^d <= 6.25e6),
+ * where U V is the tensor Chebyshev interpolant of the kernel along the cube (degree p on every
+ * axis).  Targets: host SoA (d x T).  A target touching the cube (dist <= 0) -> HB_EINVAL.
+ * Computed on the device: k2 entries for U and K, Lagrange weights per sample, DMMA GEMM. */
+hb_status hb_interpolation_decay(hb_context* ctx, const hb_kernel* kernel, const double* tgt_soa,
+                                 int64_t T, const hb_cube* cube, const int32_t* p_list,
+                                 int32_t np, double* err_out);
+/* fit_decay_rate: rho from the least-squares fit log err = log C - p log rho over the positive
+ * errors; fewer than two -> HB_EINVAL. */
+hb_status hb_fit_decay_rate(const int32_t* p, const double* err, int32_t n, double* rho_out);
+/* v_d_constant: V_d of the tensor interpolation bound; d < 1 -> HB_EINVAL, rho <= 1 -> HB_EDOMAIN. */
+hb_status hb_v_d_constant(int32_t d, double rho, double* out);
 
 /* ---- profiling: per-phase device time from CUDA events on the context stream (off by
  * default; the events add ~µs per phase) and the process-wide kernel-launch counter ---------- */

@@ -231,6 +231,14 @@ def ref_lib():
         L.hbr_classify_pair.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_int,
                                         ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
         L.hbr_box_grid.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int64, ctypes.c_void_p]
+        L.hbr_chebyshev_nodes.argtypes = [ctypes.c_int, ctypes.c_void_p]
+        L.hbr_lagrange_weights.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_double, ctypes.c_void_p]
+        L.hbr_interpolation_decay.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_double,
+                                              ctypes.c_void_p, ctypes.c_int64, ctypes.c_int,
+                                              ctypes.c_void_p, ctypes.c_double, ctypes.c_void_p,
+                                              ctypes.c_int, ctypes.c_void_p]
+        L.hbr_fit_decay_rate.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p]
+        L.hbr_v_d_constant.argtypes = [ctypes.c_int, ctypes.c_double, ctypes.c_void_p]
         for f in ("hbr_j2", "hbr_y2"):
             getattr(L, f).argtypes = [ctypes.c_double]
             getattr(L, f).restype = ctypes.c_double
@@ -301,3 +309,22 @@ def aca_compress(kernel_id: int, x: np.ndarray, y: np.ndarray, eps: float, max_r
     return ACAResult(r, bool(met.value), sigma[:r].copy(), tau[:r].copy(),
                      L[:r * r].reshape(r, r, order="F").copy(),
                      U[:r * r].reshape(r, r, order="F").copy(), b)
+
+
+def ref_interpolation_decay(kernel_id: int, x: np.ndarray, lower, side: float, p_list,
+                            has_diag: bool = True, diag: float | None = None) -> list:
+    """hodlr::interpolation_decay (chebyshev.hpp:151-177) itself, compiled from /root/reference."""
+    d, T = x.shape
+    if diag is None:
+        diag = CATALOG_DIAG.get(kernel_id, 0.0)
+    lo = np.ascontiguousarray(lower, dtype=np.float64)
+    ps = np.ascontiguousarray(p_list, dtype=np.int32)
+    out = np.zeros(len(p_list))
+    xs = np.ascontiguousarray(x)
+    st = ref_lib().hbr_interpolation_decay(kernel_id, int(has_diag), float(diag), xs.ctypes.data, T, d,
+                                           lo.ctypes.data, float(side), ps.ctypes.data, len(p_list),
+                                           out.ctypes.data)
+    if st:
+        raise OracleError(st, "hbr_interpolation_decay")
+    return list(zip(list(p_list), out.tolist()))
+

@@ -1,5 +1,5 @@
 // ref_wrap.cpp -- TEST INFRASTRUCTURE ONLY.  extern "C" wrapper that compiles the reference's
-// own headers (kernel.hpp, aca.hpp, bessel.hpp, geometry.hpp, types.hpp) from where they lie under
+// own headers (kernel.hpp, aca.hpp, bessel.hpp, geometry.hpp, chebyshev.hpp, types.hpp) from where they lie under
 // /root/reference/proj/include, against the from-scratch Eigen subset in oracle/eigen_shim,
 // into oracle/_ref/libhb_ref.so.  No reference source is copied into this repository.
 // It is the second oracle: tests pin the C restatement (hb_oracle.c) against it, and
@@ -10,6 +10,7 @@
 #include <stdexcept>
 
 #include "hodlr/aca.hpp"
+#include "hodlr/chebyshev.hpp"
 #include "hodlr/geometry.hpp"
 #include "hodlr/kernel.hpp"
 
@@ -135,6 +136,50 @@ int hbr_box_grid(int d, int level, int64_t id, int32_t* grid) {
     const Eigen::ArrayXi g = box_grid(d, level, id);
     for (int k = 0; k < d; ++k) grid[k] = g(k);
   });
+}
+
+// ---- chebyshev.hpp ------------------------------------------------------------------------
+int hbr_chebyshev_nodes(int p, double* out) {
+  return guarded([&] {
+    const Vector y = chebyshev_nodes(p);
+    for (Index i = 0; i < y.size(); ++i) out[i] = y(i);
+  });
+}
+
+int hbr_lagrange_weights(const double* nodes, int m, double y, double* out) {
+  return guarded([&] {
+    Vector nd(m);
+    for (int i = 0; i < m; ++i) nd(i) = nodes[i];
+    const Vector w = lagrange_weights(nd, y);
+    for (int i = 0; i < m; ++i) out[i] = w(i);
+  });
+}
+
+// interpolation_decay (chebyshev.hpp:151-177): max |K - U V| over the sample grid per degree.
+int hbr_interpolation_decay(int id, int has_diag, double diag, const double* x_soa, int64_t T, int d,
+                            const double* lower, double side, const int32_t* p_list, int np,
+                            double* err_out) {
+  return guarded([&] {
+    const KernelSpec s = spec_of(id, has_diag, diag);
+    Point lo(d);
+    for (int a = 0; a < d; ++a) lo(a) = lower[a];
+    const HyperCube cube(lo, side);
+    std::vector<int> ps(p_list, p_list + np);
+    const auto dec = interpolation_decay(s, soa_to_pointset(x_soa, T, d), cube, ps);
+    for (int i = 0; i < np; ++i) err_out[i] = dec[(size_t)i].second;
+  });
+}
+
+int hbr_fit_decay_rate(const int32_t* p, const double* err, int n, double* rho) {
+  return guarded([&] {
+    std::vector<std::pair<int, double>> dec;
+    for (int i = 0; i < n; ++i) dec.emplace_back(p[i], err[i]);
+    *rho = fit_decay_rate(dec);
+  });
+}
+
+int hbr_v_d_constant(int d, double rho, double* out) {
+  return guarded([&] { *out = v_d_constant(d, rho); });
 }
 
 }  // extern "C"

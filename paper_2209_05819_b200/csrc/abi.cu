@@ -546,6 +546,72 @@ hb_status hb_fit_growth(const int64_t* N, const double* rank, int32_t n, hb_grow
   });
 }
 
+hb_status hb_chebyshev_nodes(int32_t p, double* out) {
+  return guarded(nullptr, [&] {
+    if (!out) throw Error(HB_EINVAL, "chebyshev_nodes: NULL output");
+    const std::vector<double> y = hb::cheb_nodes_host(p);
+    std::memcpy(out, y.data(), sizeof(double) * y.size());
+  });
+}
+
+hb_status hb_interpolation_decay(hb_context* ctx, const hb_kernel* kernel, const double* tgt, int64_t T,
+                                 const hb_cube* cube, const int32_t* p_list, int32_t np, double* err_out) {
+  if (!ctx) return HB_EINVAL;
+  return guarded(ctx, [&] {
+    check_kernel(kernel);
+    if (!cube || !tgt || !p_list || !err_out || np < 1) throw Error(HB_EINVAL, "interpolation_decay: bad arguments");
+    check_cube(*cube);
+    if (T < 1) throw Error(HB_EINVAL, "interpolation_decay: no targets");  // chebyshev.hpp:132
+    for (int i = 0; i < np; ++i)
+      if (p_list[i] < 0) throw Error(HB_EINVAL, "chebyshev_nodes: p must be >= 0");
+    const int d = cube->d;
+    for (int64_t i = 0; i < T; ++i) {  // HyperCube::dist (geometry.hpp:46-53) > 0 (chebyshev.hpp:153-155)
+      double s = 0.0;
+      for (int k = 0; k < d; ++k) {
+        const double x = tgt[(int64_t)k * T + i];
+        const double gap = std::max({0.0, cube->lower[k] - x, x - (cube->lower[k] + cube->side)});
+        s += gap * gap;
+      }
+      if (!(std::sqrt(s) > 0.0)) throw Error(HB_EINVAL, "interpolation_decay: targets touch the cube");
+    }
+    HB_CUDA(cudaSetDevice(ctx->device));
+    hb::interpolation_decay(ctx, *kernel, tgt, T, *cube, p_list, np, err_out);
+  });
+}
+
+hb_status hb_fit_decay_rate(const int32_t* p, const double* err, int32_t n, double* rho_out) {
+  return guarded(nullptr, [&] {  // chebyshev.hpp:180-193
+    if (!p || !err || !rho_out) throw Error(HB_EINVAL, "fit_decay_rate: NULL argument");
+    double sx = 0, sy = 0, sxx = 0, sxy = 0;
+    int64_t k = 0;
+    for (int32_t i = 0; i < n; ++i) {
+      if (!(err[i] > 0)) continue;
+      const double x = p[i], y = std::log(err[i]);
+      sx += x;
+      sy += y;
+      sxx += x * x;
+      sxy += x * y;
+      ++k;
+    }
+    if (k < 2) throw Error(HB_EINVAL, "fit_decay_rate: need at least two positive errors");
+    const double slope = (k * sxy - sx * sy) / (k * sxx - sx * sx);
+    *rho_out = std::exp(-slope);
+  });
+}
+
+hb_status hb_v_d_constant(int32_t d, double rho, double* out) {
+  return guarded(nullptr, [&] {  // chebyshev.hpp:139-147
+    if (!out) throw Error(HB_EINVAL, "v_d_constant: NULL output");
+    if (d < 1) throw Error(HB_EINVAL, "v_d_constant: d must be >= 1");
+    if (!(rho > 1.0)) throw Error(HB_EDOMAIN, "v_d_constant: rho must be > 1");
+    double sum = static_cast<double>(d);
+    const double q = 1.0 - 1.0 / rho;
+    for (int l = 2; l <= d; ++l)
+      sum += std::pow(2.0, l - 1) * ((l - 1) + std::pow(2.0, l - 1) - 1.0) / std::pow(q, l - 1);
+    *out = sum;
+  });
+}
+
 hb_status hb_assemble_dense_host(hb_context* ctx, const hb_kernel* kernel, const double* tgt, int64_t T,
                                  const double* src, int64_t N, int32_t d, double* K, int64_t ldk,
                                  int64_t entry_cap) {

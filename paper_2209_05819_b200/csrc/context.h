@@ -116,5 +116,9 @@ void context_set_priority(hb_context* c, int prio);
 // free (stream-ordered, back to the device pool) every workspace buffer larger than keep_bytes
 void context_trim(hb_context* c, size_t keep_bytes);
 void context_free(hb_context* c);
+// Chebyshev bound check (chebyshev.cu, chebyshev.hpp:125-193)
+std::vector<double> cheb_nodes_host(int p);
+void interpolation_decay(hb_context* c, const hb_kernel& kern, const double* tgt_soa, int64_t T,
+                         const hb_cube& cube, const int32_t* p_list, int np, double* err_out);
 
 }  // namespace hb

@@ -130,7 +130,8 @@ EXPORTS = [
     "hb_partition", "hb_problem_seed", "hb_rank_complex", "hb_phase_name", "hb_context_set_profiling",
     "hb_stats_get", "hb_stats_reset", "hb_sweep_ex", "hb_sweep_release", "hb_context_set_stopping",
     "hb_classify_pair", "hb_classify_cubes", "hb_interaction_dprime", "hb_assemble_dense_host",
-    "hb_fit_growth",
+    "hb_fit_growth", "hb_chebyshev_nodes", "hb_interpolation_decay", "hb_fit_decay_rate",
+    "hb_v_d_constant",
     # include/hb_debug.h (test hooks)
     "hb_debug_dgemm", "hb_debug_dgemm_async", "hb_debug_dgemm_fro",
     # ACA (aca.hpp)
@@ -176,6 +177,15 @@ def load(path: os.PathLike | str | None = None):
     L.hb_fit_growth.argtypes = [ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_double),
                                 ctypes.c_int32, ctypes.POINTER(hb_growth_fit)]
     L.hb_fit_growth.restype = ctypes.c_int
+    L.hb_chebyshev_nodes.argtypes = [ctypes.c_int32, ctypes.POINTER(ctypes.c_double)]
+    L.hb_interpolation_decay.argtypes = [c_p, ctypes.POINTER(hb_kernel), c_p, ctypes.c_int64,
+                                         ctypes.POINTER(hb_cube), ctypes.POINTER(ctypes.c_int32),
+                                         ctypes.c_int32, ctypes.POINTER(ctypes.c_double)]
+    L.hb_fit_decay_rate.argtypes = [ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_double),
+                                    ctypes.c_int32, ctypes.POINTER(ctypes.c_double)]
+    L.hb_v_d_constant.argtypes = [ctypes.c_int32, ctypes.c_double, ctypes.POINTER(ctypes.c_double)]
+    for name in ("hb_chebyshev_nodes", "hb_interpolation_decay", "hb_fit_decay_rate", "hb_v_d_constant"):
+        getattr(L, name).restype = ctypes.c_int
     L.hb_interaction_dprime.argtypes = [hb_interaction]
     L.hb_interaction_dprime.restype = ctypes.c_int32
     L.hb_assemble_dense_host.argtypes = [c_p, ctypes.POINTER(hb_kernel), c_p, ctypes.c_int64, c_p,
@@ -348,6 +358,30 @@ def fit_growth(ns: Sequence[int], ranks: Sequence[float]) -> dict:
             "rss": dict(zip(GROWTH_MODELS, list(out.rss))), "max_min_ratio": out.max_min_ratio}
 
 
+def chebyshev_nodes(p: int) -> list[float]:
+    """hodlr::chebyshev_nodes (chebyshev.hpp:16-23)."""
+    out = (ctypes.c_double * max(p + 1, 1))()
+    _check(load().hb_chebyshev_nodes(p, out), "hb_chebyshev_nodes")
+    return list(out[: p + 1])
+
+
+def fit_decay_rate(ps: Sequence[int], errs: Sequence[float]) -> float:
+    """hodlr::fit_decay_rate (chebyshev.hpp:180-193)."""
+    n = len(ps)
+    cp = (ctypes.c_int32 * max(n, 1))(*ps)
+    ce = (ctypes.c_double * max(n, 1))(*errs)
+    rho = ctypes.c_double()
+    _check(load().hb_fit_decay_rate(cp, ce, n, ctypes.byref(rho)), "hb_fit_decay_rate")
+    return rho.value
+
+
+def v_d_constant(d: int, rho: float) -> float:
+    """hodlr::v_d_constant (chebyshev.hpp:139-147)."""
+    out = ctypes.c_double()
+    _check(load().hb_v_d_constant(d, rho, ctypes.byref(out)), "hb_v_d_constant")
+    return out.value
+
+
 def classify_cubes(a: hb_cube, b: hb_cube):
     out = hb_interaction()
     _check(load().hb_classify_cubes(ctypes.byref(a), ctypes.byref(b), ctypes.byref(out)),
@@ -437,6 +471,21 @@ class Context:
                                                 y.ctypes.data, N, d, K.ctypes.data, T, entry_cap),
                "hb_assemble_dense_host", self._h)
         return K
+
+    def interpolation_decay(self, kernel: hb_kernel, targets, cube: hb_cube,
+                            p_list: Sequence[int]) -> list[tuple[int, float]]:
+        """hodlr::interpolation_decay (chebyshev.hpp:151-177) on the device: (p, max entry error
+        of the degree-p tensor Chebyshev interpolant along `cube`) for each p; targets (d, T)."""
+        import numpy as np
+        x = np.ascontiguousarray(targets, dtype=np.float64)
+        d, T = x.shape
+        n = len(p_list)
+        cp = (ctypes.c_int32 * max(n, 1))(*p_list)
+        out = (ctypes.c_double * max(n, 1))()
+        _check(self._lib.hb_interpolation_decay(self._h, ctypes.byref(kernel), x.ctypes.data, T,
+                                                ctypes.byref(cube), cp, n, out),
+               "hb_interpolation_decay", self._h)
+        return list(zip(list(p_list), list(out[:n])))
 
     def rank(self, kernel: hb_kernel, pair: hb_pair, tols: Sequence[float]) -> list[RankResult]:
         nt = len(tols)
