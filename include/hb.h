@@ -26,6 +26,9 @@
  *   hb_sweep               <- SPEC rank_table + parallel_for        SPEC.md:570-578, parallel.hpp:12-29
  *   hb_fit_growth          <- SPEC fit_growth (rank vs {1, log N, N^c}) SPEC.md:580-588
  *   hb_chebyshev_nodes     <- hodlr::chebyshev_nodes                chebyshev.hpp:16-23
+ *   hb_hmatrix_build       <- hodlr::HMatrix::initialize (tree, block structure, dense leaf /
+ *                             near blocks, ACA factors)   hmatrix.hpp:50-126, cluster_tree.hpp:107-229
+ *   hb_hmatrix_matvec      <- hodlr::HMatrix::matvec                hmatrix.hpp:133-179
  *   hb_interpolation_decay <- hodlr::interpolation_decay            chebyshev.hpp:151-177
  *   hb_fit_decay_rate      <- hodlr::fit_decay_rate                 chebyshev.hpp:180-193
  *   hb_v_d_constant        <- hodlr::v_d_constant                   chebyshev.hpp:139-147
@@ -244,6 +247,38 @@ typedef struct {
   double max_min_ratio;  /* max rank / min rank of the series */
 } hb_growth_fit;
 hb_status hb_fit_growth(const int64_t* N, const double* rank, int32_t n, hb_growth_fit* out);
+
+/* ---- HODLRdD operator (hmatrix.hpp, cluster_tree.hpp) ------------------------------------------
+ * AdmissibilityPolicy (cluster_tree.hpp:17-29): which same-level box pairs are compressed. */
+enum { HB_POLICY_WEAKDD = 0, HB_POLICY_STRONG = 1, HB_POLICY_WEAKALL = 2 };
+/* BuildReport (hmatrix.hpp:19-26) */
+typedef struct {
+  double init_seconds;
+  int64_t memory_bytes;
+  int32_t max_block_rank;
+  int32_t depth;
+  int64_t num_low_rank_blocks;
+  int64_t num_dense_entries;
+  int64_t num_tolerance_failures;
+} hb_build_report;
+typedef struct hb_hmatrix hb_hmatrix; /* opaque; keeps using ctx (caller keeps it alive) */
+/* HMatrix::initialize: balanced 2^d tree over `domain` (boxes split until <= n_max points; a point
+ * on an internal face goes to the lower box), block structure of `policy`, dense leaf self and
+ * near-field blocks assembled on the device in one batched launch, admissible blocks compressed
+ * by the device ACA (epsilon, max_rank).  Points: host SoA (d x N).  Errors as the reference:
+ * epsilon <= 0, n_max < 1, max_rank < 1, N < 1, d != domain.d -> HB_EINVAL; a point outside the
+ * domain -> HB_EDOMAIN; dense entries > dense_entry_cap (0: 4e8 default) -> HB_ECAP. */
+hb_status hb_hmatrix_build(hb_context* ctx, const hb_kernel* kernel, const double* pts_soa,
+                           int64_t N, int32_t d, const hb_cube* domain, int32_t policy,
+                           int64_t n_max, double epsilon, int64_t max_rank,
+                           int64_t dense_entry_cap, hb_hmatrix** out, hb_build_report* report);
+/* b = H q in the original point ordering, for nvec host vectors (column-major N x nvec). */
+hb_status hb_hmatrix_matvec(hb_hmatrix* h, const double* q, double* b, int32_t nvec);
+/* Same on device vectors (length N), ordered on the context stream, not synchronised. */
+hb_status hb_hmatrix_matvec_device(hb_hmatrix* h, const double* d_q, double* d_b);
+/* tree id -> original point id (ClusterTree::original_id), N entries. */
+hb_status hb_hmatrix_tree_order(const hb_hmatrix* h, int64_t* orig_of_tree);
+void hb_hmatrix_destroy(hb_hmatrix* h);
 
 /* ---- Chebyshev interpolation bound check (chebyshev.hpp:125-193) --------------------------------
  * cos(pi k / p), k = 0..p (p + 1 values; p = 0 -> {0}); p < 0 -> HB_EINVAL. */

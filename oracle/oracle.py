@@ -239,6 +239,11 @@ def ref_lib():
                                               ctypes.c_int, ctypes.c_void_p]
         L.hbr_fit_decay_rate.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p]
         L.hbr_v_d_constant.argtypes = [ctypes.c_int, ctypes.c_double, ctypes.c_void_p]
+        L.hbr_hmatrix_matvec.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_void_p,
+                                         ctypes.c_int64, ctypes.c_int, ctypes.c_void_p, ctypes.c_double,
+                                         ctypes.c_int, ctypes.c_int64, ctypes.c_double, ctypes.c_int64,
+                                         ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
+                                         ctypes.c_void_p]
         for f in ("hbr_j2", "hbr_y2"):
             getattr(L, f).argtypes = [ctypes.c_double]
             getattr(L, f).restype = ctypes.c_double
@@ -327,4 +332,32 @@ def ref_interpolation_decay(kernel_id: int, x: np.ndarray, lower, side: float, p
     if st:
         raise OracleError(st, "hbr_interpolation_decay")
     return list(zip(list(p_list), out.tolist()))
+
+
+POLICIES = {"weakdd": 0, "strong": 1, "weakall": 2}  # cluster_tree.hpp:20 AdmissibilityPolicy
+
+
+def ref_hmatrix_matvec(kernel_id: int, pts: np.ndarray, lower, side: float, policy: str, n_max: int,
+                       eps: float, q: np.ndarray, max_rank: int = 1 << 14, has_diag: bool = True,
+                       diag: float | None = None):
+    """hodlr::HMatrix::initialize + matvec (hmatrix.hpp:50-179), compiled from /root/reference.
+    pts (d, N); q (N,) or (N, nq).  Returns (b, report dict, perm tree -> original)."""
+    d, N = pts.shape
+    if diag is None:
+        diag = CATALOG_DIAG.get(kernel_id, 0.0)
+    qq = np.asfortranarray(q.reshape(N, -1), dtype=np.float64)
+    b = np.zeros_like(qq)
+    rep = np.zeros(6, np.int64)
+    perm = np.zeros(N, np.int64)
+    lo = np.ascontiguousarray(lower, dtype=np.float64)
+    xs = np.ascontiguousarray(pts)
+    st = ref_lib().hbr_hmatrix_matvec(kernel_id, int(has_diag), float(diag), xs.ctypes.data, N, d,
+                                      lo.ctypes.data, float(side), POLICIES[policy], n_max, float(eps),
+                                      max_rank, qq.ctypes.data, qq.shape[1], b.ctypes.data,
+                                      rep.ctypes.data, perm.ctypes.data)
+    if st:
+        raise OracleError(st, "hbr_hmatrix_matvec")
+    keys = ["max_block_rank", "num_low_rank_blocks", "num_dense_entries", "num_tolerance_failures",
+            "memory_bytes", "depth"]
+    return b.reshape(q.shape), dict(zip(keys, rep.tolist())), perm
 

@@ -1,5 +1,6 @@
 // ref_wrap.cpp -- TEST INFRASTRUCTURE ONLY.  extern "C" wrapper that compiles the reference's
-// own headers (kernel.hpp, aca.hpp, bessel.hpp, geometry.hpp, chebyshev.hpp, types.hpp) from where they lie under
+// own headers (kernel.hpp, aca.hpp, bessel.hpp, geometry.hpp, chebyshev.hpp, cluster_tree.hpp,
+// hmatrix.hpp, types.hpp) from where they lie under
 // /root/reference/proj/include, against the from-scratch Eigen subset in oracle/eigen_shim,
 // into oracle/_ref/libhb_ref.so.  No reference source is copied into this repository.
 // It is the second oracle: tests pin the C restatement (hb_oracle.c) against it, and
@@ -12,6 +13,7 @@
 #include "hodlr/aca.hpp"
 #include "hodlr/chebyshev.hpp"
 #include "hodlr/geometry.hpp"
+#include "hodlr/hmatrix.hpp"
 #include "hodlr/kernel.hpp"
 
 using namespace hodlr;
@@ -180,6 +182,40 @@ int hbr_fit_decay_rate(const int32_t* p, const double* err, int n, double* rho) 
 
 int hbr_v_d_constant(int d, double rho, double* out) {
   return guarded([&] { *out = v_d_constant(d, rho); });
+}
+
+// ---- cluster_tree.hpp / hmatrix.hpp ---------------------------------------------------------
+// HMatrix::initialize (hmatrix.hpp:50-126) + matvec (hmatrix.hpp:133-179) on nq vectors
+// (column-major N x nq), single-threaded.  report: [max_block_rank, num_low_rank_blocks,
+// num_dense_entries, num_tolerance_failures, memory_bytes, depth].  perm: tree -> original id.
+int hbr_hmatrix_matvec(int id, int has_diag, double diag, const double* pts_soa, int64_t N, int d,
+                       const double* lower, double side, int policy, int64_t n_max, double eps,
+                       int64_t max_rank, const double* q, int nq, double* b, int64_t* report,
+                       int64_t* perm) {
+  return guarded([&] {
+    const KernelSpec s = spec_of(id, has_diag, diag);
+    Point lo(d);
+    for (int a = 0; a < d; ++a) lo(a) = lower[a];
+    const HyperCube dom(lo, side);
+    HMatrixOptions opts;
+    opts.max_rank = max_rank;
+    auto [h, rep] = HMatrix::initialize(soa_to_pointset(pts_soa, N, d), dom, s,
+                                        static_cast<AdmissibilityPolicy>(policy), n_max, eps, opts);
+    for (int c = 0; c < nq; ++c) {
+      Vector qq(N);
+      for (int64_t i = 0; i < N; ++i) qq(i) = q[i + c * N];
+      const Vector bb = h.matvec(qq);
+      for (int64_t i = 0; i < N; ++i) b[i + c * N] = bb(i);
+    }
+    report[0] = rep.max_block_rank;
+    report[1] = rep.num_low_rank_blocks;
+    report[2] = rep.num_dense_entries;
+    report[3] = rep.num_tolerance_failures;
+    report[4] = rep.memory_bytes;
+    report[5] = h.tree().depth();
+    if (perm)
+      for (int64_t t = 0; t < N; ++t) perm[t] = h.tree().original_id(t);
+  });
 }
 
 }  // extern "C"

@@ -12,5 +12,5 @@ from .hb import (  # noqa: F401
     problem_seed, sweep, global_stats, reset_global_stats, sweep_release, hb_stats, PHASES,
     ACAFactor, hb_block, classify_pair, classify_cubes, hb_interaction, hb_cube, IC_SELF,
     IC_SURFACE, IC_FAR, DPRIME_FAR, DPRIME_SELF, fit_growth,
-    chebyshev_nodes, fit_decay_rate, v_d_constant,
+    chebyshev_nodes, fit_decay_rate, v_d_constant, HMatrix, hb_build_report, POLICIES,
 )

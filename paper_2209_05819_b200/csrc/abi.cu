@@ -14,6 +14,7 @@
 
 #include "context.h"
 #include "bessel_dd.cuh"
+#include "hmatrix.h"
 
 namespace {
 
@@ -544,6 +545,92 @@ hb_status hb_fit_growth(const int64_t* N, const double* rank, int32_t n, hb_grow
     }
     *out = f;
   });
+}
+
+hb_status hb_hmatrix_build(hb_context* ctx, const hb_kernel* kernel, const double* pts, int64_t N, int32_t d,
+                           const hb_cube* domain, int32_t policy, int64_t n_max, double epsilon,
+                           int64_t max_rank, int64_t dense_entry_cap, hb_hmatrix** out,
+                           hb_build_report* report) {
+  if (!ctx || !out) return HB_EINVAL;
+  *out = nullptr;
+  hb_hmatrix* h = nullptr;
+  const hb_status s = guarded(ctx, [&] {
+    check_kernel(kernel);
+    if (!(epsilon > 0)) throw Error(HB_EINVAL, "HMatrix: epsilon must be positive");  // hmatrix.hpp:56
+    if (!pts || !domain) throw Error(HB_EINVAL, "HMatrix: NULL argument");
+    if (N < 1) throw Error(HB_EINVAL, "build_tree: empty point set");  // cluster_tree.hpp:185
+    if (n_max < 1) throw Error(HB_EINVAL, "build_tree: n_max must be >= 1");
+    if (max_rank < 1) throw Error(HB_EINVAL, "aca::compress: max_rank must be >= 1");
+    if (policy < HB_POLICY_WEAKDD || policy > HB_POLICY_WEAKALL) throw Error(HB_EINVAL, "unknown policy");
+    check_cube(*domain);
+    if (d != domain->d) throw Error(HB_EINVAL, "build_tree: point dimension does not match domain");
+    for (int64_t i = 0; i < N; ++i)  // HyperCube::contains, closed bounds (geometry.hpp:39-44)
+      for (int k = 0; k < d; ++k) {
+        const double x = pts[(int64_t)k * N + i];
+        if (x < domain->lower[k] || x > domain->lower[k] + domain->side)
+          throw Error(HB_EDOMAIN, "build_tree: point outside the domain hyper-cube");
+      }
+    HB_CUDA(cudaSetDevice(ctx->device));
+    h = new hb_hmatrix();
+    h->ctx = ctx;
+    h->device = ctx->device;
+    h->kern = *kernel;
+    h->d = d;
+    h->N = N;
+    h->policy = policy;
+    hb::hmatrix_build(h, pts, *domain, n_max, epsilon, max_rank,
+                      dense_entry_cap > 0 ? dense_entry_cap : 400000000ll);
+    if (report) *report = h->report;
+  });
+  if (s != HB_OK) {
+    if (h) {
+      hb::hmatrix_free(h);
+      delete h;
+    }
+    return s;
+  }
+  *out = h;
+  return HB_OK;
+}
+
+hb_status hb_hmatrix_matvec_device(hb_hmatrix* h, const double* d_q, double* d_b) {
+  if (!h || !d_q || !d_b) return HB_EINVAL;
+  return guarded(h->ctx, [&] {
+    HB_CUDA(cudaSetDevice(h->ctx->device));
+    hb::hmatrix_matvec(h, d_q, d_b);
+  });
+}
+
+hb_status hb_hmatrix_matvec(hb_hmatrix* h, const double* q, double* b, int32_t nvec) {
+  if (!h || !q || !b || nvec < 1) return HB_EINVAL;
+  return guarded(h->ctx, [&] {
+    hb_context* c = h->ctx;
+    HB_CUDA(cudaSetDevice(c->device));
+    const int64_t n = h->N;
+    double* dq = hb::ws<double>(c, hb::B_PX, (size_t)n);
+    double* db = hb::ws<double>(c, hb::B_PY, (size_t)n);
+    for (int32_t v = 0; v < nvec; ++v) {
+      HB_CUDA(cudaMemcpyAsync(dq, q + (int64_t)v * n, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
+      hb::hmatrix_matvec(h, dq, db);
+      HB_CUDA(cudaMemcpyAsync(b + (int64_t)v * n, db, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
+    }
+    unsigned int f = 0;
+    HB_CUDA(cudaMemcpyAsync(&f, h->d_flags, sizeof(f), cudaMemcpyDeviceToHost, c->stream));
+    HB_CUDA(cudaStreamSynchronize(c->stream));
+    raise_flags(f);
+  });
+}
+
+hb_status hb_hmatrix_tree_order(const hb_hmatrix* h, int64_t* orig) {
+  if (!h || !orig) return HB_EINVAL;
+  std::memcpy(orig, h->orig_of_tree.data(), sizeof(int64_t) * h->N);
+  return HB_OK;
+}
+
+void hb_hmatrix_destroy(hb_hmatrix* h) {
+  if (!h) return;
+  hb::hmatrix_free(h);
+  delete h;
 }
 
 hb_status hb_chebyshev_nodes(int32_t p, double* out) {

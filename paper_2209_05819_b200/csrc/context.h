@@ -116,6 +116,11 @@ void context_set_priority(hb_context* c, int prio);
 // free (stream-ordered, back to the device pool) every workspace buffer larger than keep_bytes
 void context_trim(hb_context* c, size_t keep_bytes);
 void context_free(hb_context* c);
+// HODLRdD operator (hmatrix.cu)
+void hmatrix_build(hb_hmatrix* h, const double* pts_soa, const hb_cube& dom, int64_t n_max, double eps,
+                   int64_t max_rank, int64_t dense_cap);
+void hmatrix_matvec(hb_hmatrix* h, const double* d_q, double* d_b);
+void hmatrix_free(hb_hmatrix* h);
 // Chebyshev bound check (chebyshev.cu, chebyshev.hpp:125-193)
 std::vector<double> cheb_nodes_host(int p);
 void interpolation_decay(hb_context* c, const hb_kernel& kern, const double* tgt_soa, int64_t T,

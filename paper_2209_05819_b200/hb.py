@@ -117,6 +117,20 @@ class hb_growth_fit(ctypes.Structure):
 GROWTH_MODELS = ["constant", "log", "power"]
 
 
+class hb_build_report(ctypes.Structure):
+    """BuildReport (hmatrix.hpp:19-26)."""
+    _fields_ = [("init_seconds", ctypes.c_double), ("memory_bytes", ctypes.c_int64),
+                ("max_block_rank", ctypes.c_int32), ("depth", ctypes.c_int32),
+                ("num_low_rank_blocks", ctypes.c_int64), ("num_dense_entries", ctypes.c_int64),
+                ("num_tolerance_failures", ctypes.c_int64)]
+
+    def as_dict(self) -> dict:
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+POLICIES = {"weakdd": 0, "strong": 1, "weakall": 2}  # AdmissibilityPolicy (cluster_tree.hpp:17-29)
+
+
 class hb_problem(ctypes.Structure):
     _fields_ = [("kernel", hb_kernel), ("pair", hb_pair), ("tols", ctypes.c_double * MAX_TOLS),
                 ("ntol", ctypes.c_int32), ("reserved", ctypes.c_int32)]
@@ -131,7 +145,8 @@ EXPORTS = [
     "hb_stats_get", "hb_stats_reset", "hb_sweep_ex", "hb_sweep_release", "hb_context_set_stopping",
     "hb_classify_pair", "hb_classify_cubes", "hb_interaction_dprime", "hb_assemble_dense_host",
     "hb_fit_growth", "hb_chebyshev_nodes", "hb_interpolation_decay", "hb_fit_decay_rate",
-    "hb_v_d_constant",
+    "hb_v_d_constant", "hb_hmatrix_build", "hb_hmatrix_matvec", "hb_hmatrix_matvec_device",
+    "hb_hmatrix_tree_order", "hb_hmatrix_destroy",
     # include/hb_debug.h (test hooks)
     "hb_debug_dgemm", "hb_debug_dgemm_async", "hb_debug_dgemm_fro",
     # ACA (aca.hpp)
@@ -177,6 +192,18 @@ def load(path: os.PathLike | str | None = None):
     L.hb_fit_growth.argtypes = [ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_double),
                                 ctypes.c_int32, ctypes.POINTER(hb_growth_fit)]
     L.hb_fit_growth.restype = ctypes.c_int
+    L.hb_hmatrix_build.argtypes = [c_p, ctypes.POINTER(hb_kernel), c_p, ctypes.c_int64, ctypes.c_int32,
+                                   ctypes.POINTER(hb_cube), ctypes.c_int32, ctypes.c_int64,
+                                   ctypes.c_double, ctypes.c_int64, ctypes.c_int64, ctypes.POINTER(c_p),
+                                   ctypes.POINTER(hb_build_report)]
+    L.hb_hmatrix_matvec.argtypes = [c_p, c_p, c_p, ctypes.c_int32]
+    L.hb_hmatrix_matvec_device.argtypes = [c_p, c_p, c_p]
+    L.hb_hmatrix_tree_order.argtypes = [c_p, c_p]
+    L.hb_hmatrix_destroy.argtypes = [c_p]
+    L.hb_hmatrix_destroy.restype = None
+    for name in ("hb_hmatrix_build", "hb_hmatrix_matvec", "hb_hmatrix_matvec_device",
+                 "hb_hmatrix_tree_order"):
+        getattr(L, name).restype = ctypes.c_int
     L.hb_chebyshev_nodes.argtypes = [ctypes.c_int32, ctypes.POINTER(ctypes.c_double)]
     L.hb_interpolation_decay.argtypes = [c_p, ctypes.POINTER(hb_kernel), c_p, ctypes.c_int64,
                                          ctypes.POINTER(hb_cube), ctypes.POINTER(ctypes.c_int32),
@@ -571,6 +598,57 @@ class Context:
         _check(self._lib.hb_last_sigma(self._h, buf, k, ctypes.byref(cnt)), "hb_last_sigma",
                self._h)
         return list(buf[:k])
+
+
+class HMatrix:
+    """HODLRdD operator on the device (hmatrix.hpp:50-179): hodlr::HMatrix::initialize + matvec.
+    points: (d, N) host array; domain: hb_cube; policy: "weakdd" | "strong" | "weakall"."""
+
+    def __init__(self, ctx: "Context", kernel: hb_kernel, points, domain: hb_cube,
+                 policy: str = "weakdd", n_max: int = 1000, epsilon: float = 1e-6,
+                 max_rank: int = 1 << 14, dense_entry_cap: int = 0):
+        import numpy as np
+        self._lib = load()
+        self._ctx = ctx  # the operator runs on (and keeps) this context
+        x = np.ascontiguousarray(points, dtype=np.float64)
+        self.d, self.n = x.shape
+        self._h = ctypes.c_void_p()
+        rep = hb_build_report()
+        _check(self._lib.hb_hmatrix_build(ctx._h, ctypes.byref(kernel), x.ctypes.data, self.n, self.d,
+                                          ctypes.byref(domain), POLICIES[policy], n_max, epsilon,
+                                          max_rank, dense_entry_cap, ctypes.byref(self._h),
+                                          ctypes.byref(rep)), "hb_hmatrix_build", ctx._h)
+        self.report = rep.as_dict()
+
+    def matvec(self, q):
+        """b = H q in the original ordering; q of shape (N,) or (N, nvec)."""
+        import numpy as np
+        qq = np.asfortranarray(np.asarray(q, dtype=np.float64).reshape(self.n, -1))
+        b = np.zeros_like(qq)
+        _check(self._lib.hb_hmatrix_matvec(self._h, qq.ctypes.data, b.ctypes.data, qq.shape[1]),
+               "hb_hmatrix_matvec", self._ctx._h)
+        return b.reshape(np.shape(q))
+
+    def matvec_device(self, d_q: int, d_b: int):
+        _check(self._lib.hb_hmatrix_matvec_device(self._h, d_q, d_b), "hb_hmatrix_matvec_device",
+               self._ctx._h)
+
+    def tree_order(self):
+        import numpy as np
+        out = np.zeros(self.n, np.int64)
+        _check(self._lib.hb_hmatrix_tree_order(self._h, out.ctypes.data), "hb_hmatrix_tree_order")
+        return out
+
+    def close(self):
+        if self._h:
+            self._lib.hb_hmatrix_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 class ACAFactor:
