@@ -10,6 +10,11 @@
 //   hb200::BoxIndex, classify_pair       <- hodlr::BoxIndex, classify_pair (geometry.hpp:66-71, 106-118)
 //   hb200::assemble_dense                <- hodlr::assemble_dense (kernel.hpp:168-181), host
 //                                           PointSets in, host column-major Matrix out
+//   hb200::HMatrix, BuildReport, AdmissibilityPolicy
+//        <- hodlr::HMatrix::initialize / matvec (hmatrix.hpp:19-179, cluster_tree.hpp:17-29)
+//   hb200::chebyshev_nodes, interpolation_decay, fit_decay_rate, v_d_constant
+//        <- chebyshev.hpp:16-23, 139-193
+//   hb200::fit_growth                    <- SPEC fit_growth
 //   hb200::pair_geometry, epsilon_rank, rank_table, RankRecord, write_csv
 //        <- SPEC rankbench module (CSV schema SPEC.md:613)
 // Exceptions follow the reference: std::invalid_argument (HB_EINVAL), std::length_error
@@ -499,4 +504,87 @@ inline void apply(Device& dev, const ACAFactor& f, const BlockSpec& block, const
         "aca::apply", dev.get());
 }
 
+// ---- HODLRdD operator (hmatrix.hpp) ----------------------------------------------------------
+enum class AdmissibilityPolicy { WeakDD = HB_POLICY_WEAKDD, Strong = HB_POLICY_STRONG, WeakAll = HB_POLICY_WEAKALL };
+using BuildReport = hb_build_report;  // hmatrix.hpp:19-26
+
+// HMatrix::initialize + matvec on the device: the tree, block structure, dense leaf / near blocks
+// and ACA factors live on the device of `dev` (which must outlive the operator).
+class HMatrix {
+ public:
+  static std::pair<HMatrix, BuildReport> initialize(Device& dev, const PointSet& points, const HyperCube& domain,
+                                                    const KernelSpec& kernel, AdmissibilityPolicy policy,
+                                                    int64_t n_max, double epsilon, int64_t max_rank = 1 << 14,
+                                                    int64_t dense_entry_cap = 400'000'000) {
+    HMatrix h;
+    h.n_ = points.n;
+    const hb_kernel ck = kernel.to_c();
+    const hb_cube cd = domain.to_c();
+    BuildReport rep{};
+    hb_hmatrix* raw = nullptr;
+    check(hb_hmatrix_build(dev.get(), &ck, points.soa.data(), points.n, points.d, &cd, (int32_t)policy, n_max,
+                           epsilon, max_rank, dense_entry_cap, &raw, &rep),
+          "HMatrix::initialize", dev.get());
+    h.h_.reset(raw, [](hb_hmatrix* p) { hb_hmatrix_destroy(p); });
+    h.dev_ = dev.get();
+    return {std::move(h), rep};
+  }
+  int64_t size() const { return n_; }
+  // b = K q in the original point ordering (hmatrix.hpp:133-179)
+  std::vector<double> matvec(const std::vector<double>& q) const {
+    if ((int64_t)q.size() != n_) throw std::invalid_argument("HMatrix::matvec: length mismatch");
+    std::vector<double> b((size_t)n_);
+    check(hb_hmatrix_matvec(h_.get(), q.data(), b.data(), 1), "HMatrix::matvec", dev_);
+    return b;
+  }
+  int64_t original_id(int64_t tree_id) const {  // ClusterTree::original_id
+    std::vector<int64_t> o((size_t)n_);
+    check(hb_hmatrix_tree_order(h_.get(), o.data()), "HMatrix::original_id");
+    return o.at((size_t)tree_id);
+  }
+
+ private:
+  std::shared_ptr<hb_hmatrix> h_;
+  hb_context* dev_ = nullptr;
+  int64_t n_ = 0;
+};
+
+// ---- Chebyshev interpolation bound check (chebyshev.hpp:16-23, 139-193) ---------------------
+inline std::vector<double> chebyshev_nodes(int p) {
+  std::vector<double> y((size_t)std::max(p + 1, 1));
+  check(hb_chebyshev_nodes(p, y.data()), "chebyshev_nodes");
+  return y;
+}
+inline std::vector<std::pair<int, double>> interpolation_decay(Device& dev, const KernelSpec& spec,
+                                                               const PointSet& targets, const HyperCube& cube,
+                                                               const std::vector<int>& p_list) {
+  const hb_kernel ck = spec.to_c();
+  const hb_cube cc = cube.to_c();
+  std::vector<int32_t> ps(p_list.begin(), p_list.end());
+  std::vector<double> err(ps.size());
+  check(hb_interpolation_decay(dev.get(), &ck, targets.soa.data(), targets.n, &cc, ps.data(), (int32_t)ps.size(),
+                               err.data()),
+        "interpolation_decay", dev.get());
+  std::vector<std::pair<int, double>> out;
+  for (size_t i = 0; i < ps.size(); ++i) out.emplace_back(ps[i], err[i]);
+  return out;
+}
+inline double fit_decay_rate(const std::vector<std::pair<int, double>>& decay) {
+  std::vector<int32_t> p;
+  std::vector<double> e;
+  for (const auto& [pp, ee] : decay) {
+    p.push_back(pp);
+    e.push_back(ee);
+  }
+  double rho = 0.0;
+  check(hb_fit_decay_rate(p.data(), e.data(), (int32_t)p.size(), &rho), "fit_decay_rate");
+  return rho;
+}
+inline double v_d_constant(int d, double rho) {
+  double v = 0.0;
+  check(hb_v_d_constant(d, rho, &v), "v_d_constant");
+  return v;
+}
+
 }  // namespace hb200
+
