@@ -1096,6 +1096,8 @@ hb_status hb_sweep_ex(const hb_problem* probs, int64_t n, const int32_t* devices
         // rest (caps sum to <= num_sms, so co-resident barriers cannot deadlock)
         int lo = 0, hi = 0;
         cudaDeviceGetStreamPriorityRange(&lo, &hi);
+        static const bool no_prio = getenv("HB_NO_PRIORITY") != nullptr;  // experiments
+        if (no_prio) hi = lo;
         try {
           hb::context_set_priority(sc, (s == 0 && nsub > 1) ? hi : lo);
         } catch (const hb::Error&) {

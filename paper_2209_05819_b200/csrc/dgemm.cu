@@ -425,7 +425,7 @@ __global__ void gemm_check_diff(const double* C, int64_t ldc, const double* D, i
   atomicMax(reinterpret_cast<unsigned long long*>(out + 1), __double_as_longlong(ref));
 }
 
-void launch_dgemm(const GemmArgs& g, double* ws, int64_t ws_elems, int num_sms, cudaStream_t st);
+static void launch_dgemm_cpasync(const GemmArgs& g, double* ws, int64_t ws_elems, int num_sms, cudaStream_t st);
 
 static void checked_tma(const GemmArgs& g, double* ws, int64_t ws_elems, int num_sms, cudaStream_t st) {
   double *D = nullptr, *F = nullptr, *out = nullptr;
@@ -440,9 +440,7 @@ static void checked_tma(const GemmArgs& g, double* ws, int64_t ws_elems, int num
   r.ldc = g.M;
   r.fro_partials = g.fro_partials ? F : nullptr;
   launch_dgemm_tma(g, num_sms, st);
-  setenv("HB_GEMM_TMA_FORCE_OFF", "1", 1);
-  launch_dgemm(r, ws, ws_elems, num_sms, st);
-  unsetenv("HB_GEMM_TMA_FORCE_OFF");
+  launch_dgemm_cpasync(r, ws, ws_elems, num_sms, st);
   gemm_check_diff<<<296, 256, 0, st>>>(g.C, g.ldc, D, g.M, g.N, out);
   std::vector<double> hp(cnt), hq(cnt);
   double h[2];
@@ -473,7 +471,7 @@ static void checked_tma(const GemmArgs& g, double* ws, int64_t ws_elems, int num
 void launch_dgemm(const GemmArgs& g, double* ws, int64_t ws_elems, int num_sms, cudaStream_t st) {
   if (g.M <= 0 || g.N <= 0) return;
   static const bool check = getenv("HB_GEMM_CHECK") != nullptr;
-  if (tma_gemm_eligible(g) && !getenv("HB_GEMM_TMA_FORCE_OFF")) {
+  if (tma_gemm_eligible(g)) {
     if (check) {
       checked_tma(g, ws, ws_elems, num_sms, st);
       if (g.fro_partials) {
@@ -493,6 +491,12 @@ void launch_dgemm(const GemmArgs& g, double* ws, int64_t ws_elems, int num_sms, 
     }
     return;
   }
+  launch_dgemm_cpasync(g, ws, ws_elems, num_sms, st);
+}
+
+// The cp.async DMMA kernel (every shape; the product path for the trailing update too).
+static void launch_dgemm_cpasync(const GemmArgs& g, double* ws, int64_t ws_elems, int num_sms, cudaStream_t st) {
+  if (g.M <= 0 || g.N <= 0) return;
   GemmParams p{};
   p.M = g.M; p.N = g.N; p.K = g.K;
   p.alpha = g.alpha; p.beta = g.beta;
