@@ -17,6 +17,9 @@
 // Frobenius norm of the trailing matrix A22, used by the QR stopping rule), written in a fixed
 // order so the result is deterministic.  Split-K (for skinny outputs with a long reduction)
 // writes per-slice partials that a second kernel sums in a fixed order.
+#include <cstring>
+#include <string>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -426,6 +429,38 @@ __global__ void gemm_check_diff(const double* C, int64_t ldc, const double* D, i
 }
 
 static void launch_dgemm_cpasync(const GemmArgs& g, double* ws, int64_t ws_elems, int num_sms, cudaStream_t st);
+int tma_gemm_strip(int64_t M, int64_t N, int num_sms);
+
+// Diagnostics of a flagged update: the first bad elements with the three 40-deep chunk products
+// of their own column and of the same column of the neighbouring tiles (c -+ 64), to tell a stale
+// or missing ring chunk from a wrong C value.  out: [0] = count, then 12 doubles per element.
+__global__ void gemm_check_diag(const double* C, int64_t ldc, const double* D, int64_t M, int64_t N,
+                                const double* A, int64_t lda, const double* B, int64_t ldb, int64_t K,
+                                double tol, double* out, int max_out, unsigned long long* hist) {
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < M * N;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t m = idx % M, n = idx / M;
+    const double a = C[m + n * ldc], b = D[idx];
+    if (!(fabs(a - b) <= tol)) {
+      atomicAdd(&hist[m % 128], 1ull);          // row inside the m-block
+      atomicAdd(&hist[128 + n % 64], 1ull);     // column inside the tile
+      const int slot = (int)atomicAdd(reinterpret_cast<unsigned long long*>(out), 1ull);
+      if (slot < max_out) {
+        double* o = out + 1 + slot * 12;
+        o[0] = (double)m; o[1] = (double)n; o[2] = a - b;
+        for (int w = 0; w < 3; ++w) {
+          const int64_t nn = n + (w - 1) * 64;
+          for (int ch = 0; ch < 3; ++ch) {
+            double s = 0.0;
+            if (nn >= 0 && nn < N)
+              for (int64_t k = ch * 40; k < min((int64_t)(ch + 1) * 40, K); ++k) s += A[m + k * lda] * B[k + nn * ldb];
+            o[3 + w * 3 + ch] = s;
+          }
+        }
+      }
+    }
+  }
+}
 
 static void checked_tma(const GemmArgs& g, double* ws, int64_t ws_elems, int num_sms, cudaStream_t st) {
   double *D = nullptr, *F = nullptr, *out = nullptr;
@@ -439,7 +474,11 @@ static void checked_tma(const GemmArgs& g, double* ws, int64_t ws_elems, int num
   r.C = D;
   r.ldc = g.M;
   r.fro_partials = g.fro_partials ? F : nullptr;
-  launch_dgemm_tma(g, num_sms, st);
+  // control (HB_GEMM_CHECK=2): the primary run is the cp.async kernel too, so any flag then comes
+  // from the check itself or from operands changing under it, not from the TMA kernel
+  static const bool control = atoi(getenv("HB_GEMM_CHECK")) == 2;
+  if (control) launch_dgemm_cpasync(g, ws, ws_elems, num_sms, st);
+  else launch_dgemm_tma(g, num_sms, st);
   launch_dgemm_cpasync(r, ws, ws_elems, num_sms, st);
   gemm_check_diff<<<296, 256, 0, st>>>(g.C, g.ldc, D, g.M, g.N, out);
   std::vector<double> hp(cnt), hq(cnt);
@@ -458,10 +497,44 @@ static void checked_tma(const GemmArgs& g, double* ws, int64_t ws_elems, int num
               (long long)g.N, (long long)g.K, a, b);
   }
   HB_CUDA(cudaStreamSynchronize(st));
-  if (!(h[0] <= 1e-13 * h[1]))
+  if (!(h[0] <= 1e-13 * h[1])) {
     fprintf(stderr, "[gemm check] C M=%lld N=%lld K=%lld lda=%lld ldb=%lld ldc=%lld A=%p B=%p C=%p: maxdiff %.3g ref %.3g\n",
             (long long)g.M, (long long)g.N, (long long)g.K, (long long)g.lda, (long long)g.ldb,
             (long long)g.ldc, (const void*)g.A, (const void*)g.B, (void*)g.C, h[0], h[1]);
+    constexpr int kMax = 6;
+    double* dg = nullptr;
+    unsigned long long* hist = nullptr;
+    HB_CUDA(cudaMallocAsync(&dg, sizeof(double) * (1 + 12 * kMax), st));
+    HB_CUDA(cudaMallocAsync(&hist, sizeof(unsigned long long) * 192, st));
+    HB_CUDA(cudaMemsetAsync(dg, 0, sizeof(double) * (1 + 12 * kMax), st));
+    HB_CUDA(cudaMemsetAsync(hist, 0, sizeof(unsigned long long) * 192, st));
+    gemm_check_diag<<<296, 256, 0, st>>>(g.C, g.ldc, D, g.M, g.N, g.A, g.lda, g.B, g.ldb, g.K,
+                                         1e-13 * h[1], dg, kMax, hist);
+    double hd[1 + 12 * kMax];
+    unsigned long long hh[192];
+    HB_CUDA(cudaMemcpyAsync(hd, dg, sizeof(hd), cudaMemcpyDeviceToHost, st));
+    HB_CUDA(cudaMemcpyAsync(hh, hist, sizeof(hh), cudaMemcpyDeviceToHost, st));
+    HB_CUDA(cudaStreamSynchronize(st));
+    unsigned long long cnt_bad;
+    memcpy(&cnt_bad, &hd[0], 8);
+    const int strip = tma_gemm_strip(g.M, g.N, num_sms);
+    std::string line = "[gemm diag] bad " + std::to_string(cnt_bad) + " strip " + std::to_string(strip) +
+                       " mblocks " + std::to_string((g.M + 127) / 128) + " rows%128:";
+    for (int i = 0; i < 128; ++i) if (hh[i]) line += " " + std::to_string(i) + "x" + std::to_string(hh[i]);
+    line += " cols%64:";
+    for (int i = 0; i < 64; ++i) if (hh[128 + i]) line += " " + std::to_string(i) + "x" + std::to_string(hh[128 + i]);
+    fprintf(stderr, "%s\n", line.c_str());
+    for (int e = 0; e < (int)std::min<unsigned long long>(cnt_bad, kMax); ++e) {
+      const double* o = hd + 1 + e * 12;
+      fprintf(stderr, "[gemm diag]  r=%lld (mb %lld, row %lld) c=%lld (tile %lld, in-strip %lld, col %lld): got-want %+.4e; "
+              "chunk products own %+.4e %+.4e %+.4e | c-64 %+.4e %+.4e %+.4e | c+64 %+.4e %+.4e %+.4e\n",
+              (long long)o[0], (long long)o[0] / 128, (long long)o[0] % 128, (long long)o[1],
+              (long long)o[1] / 64, ((long long)o[1] / 64) % strip, (long long)o[1] % 64, o[2], o[6], o[7], o[8],
+              o[3], o[4], o[5], o[9], o[10], o[11]);
+    }
+    HB_CUDA(cudaFreeAsync(dg, st));
+    HB_CUDA(cudaFreeAsync(hist, st));
+  }
   // the caller's C must hold the TMA result (already there); the check buffers go back
   HB_CUDA(cudaFreeAsync(D, st));
   HB_CUDA(cudaFreeAsync(F, st));
@@ -474,7 +547,7 @@ void launch_dgemm(const GemmArgs& g, double* ws, int64_t ws_elems, int num_sms, 
   if (tma_gemm_eligible(g)) {
     if (check) {
       checked_tma(g, ws, ws_elems, num_sms, st);
-      if (g.fro_partials) {
+      if (g.fro_partials && atoi(getenv("HB_GEMM_CHECK")) != 2) {
         const int64_t written = tma_gemm_fro_count(g.M, g.N, num_sms);
         const int64_t cnt = gemm_fro_count(g.M, g.N, g.K, num_sms);
         if (cnt > written)
