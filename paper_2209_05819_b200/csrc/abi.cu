@@ -271,10 +271,60 @@ double predicted_rank(int d, int dprime, int64_t n) {
   return std::min<double>((double)n, base * std::pow((double)n / n0, (double)dprime / d));
 }
 
+// Factorisation width k̂ (columns of the pivoted QR before certification).  For the three BASELINE
+// kernels and d <= 4 it is interpolated geometrically in N between the widths measured at
+// N = 1000, 8000 and 65536 (tol 1e-12; profiles/r02/solo_all_s3a.json); any other problem falls back
+// to 1.4 p̂ + 32 from the paper's growth laws.  Scheduling only: a wrong k̂ costs balance, never a
+// result.
+double predicted_width(const hb_problem& p) {
+  struct Row { int d, dp; double k[3][3]; };  // k[kernel: 1/r, log r, exp(-r)][N = 1000, 8000, 65536]
+  static const Row tab[] = {
+      {1, -1, {{16, 16, 16}, {8, 8, 8}, {8, 8, 8}}},
+      {1, 0, {{32, 40, 48}, {24, 32, 40}, {8, 8, 8}}},
+      {2, -1, {{64, 64, 64}, {24, 24, 32}, {56, 56, 56}}},
+      {2, 0, {{112, 152, 192}, {48, 56, 64}, {96, 120, 144}}},
+      {2, 1, {{232, 616, 1680}, {120, 272, 696}, {200, 480, 1200}}},
+      {3, -1, {{176, 208, 216}, {256, 312, 328}, {232, 280, 288}}},
+      {3, 0, {{216, 312, 432}, {320, 480, 600}, {280, 408, 560}}},
+      {3, 1, {{296, 576, 1080}, {432, 888, 1680}, {360, 696, 1200}}},
+      {3, 2, {{472, 1560, 5752}, {624, 2152, 7800}, {536, 1744, 6120}}},
+      {4, -1, {{704, 1552, 2040}, {664, 1320, 1680}, {712, 1512, 1800}}},
+      {4, 0, {{712, 1536, 2280}, {672, 1320, 1912}, {720, 1440, 2128}}},
+      {4, 1, {{784, 2080, 3840}, {752, 1848, 3240}, {784, 1976, 3360}}},
+      {4, 2, {{888, 3000, 8520}, {872, 2760, 6960}, {880, 2832, 6960}}},
+      {4, 3, {{960, 4504, 19800}, {960, 4320, 18120}, {952, 4312, 17880}}},
+  };
+  const double n = (double)std::max(p.pair.n_target, p.pair.n_source);
+  const int d = p.pair.target.d, dp = p.pair.d_prime < 0 ? -1 : p.pair.d_prime;
+  const int kc = p.kernel.id == HB_K_INVERSE_R ? 0 : (p.kernel.id == HB_K_LOG_R ? 1 : (p.kernel.id == HB_K_EXP_NEG_R ? 2 : -1));
+  if (kc >= 0)
+    for (const Row& r : tab)
+      if (r.d == d && r.dp == dp) {
+        const int hi = n > 8000.0 ? 1 : 0;  // piecewise geometric: [1000, 8000], [8000, 65536]
+        const double n0 = hi ? 8000.0 : 1000.0, n1 = hi ? 65536.0 : 8000.0;
+        const double g = std::log(r.k[kc][hi + 1] / r.k[kc][hi]) / std::log(n1 / n0);
+        return std::min(n, r.k[kc][hi] * std::pow(std::max(n, 64.0) / n0, g));
+      }
+  return std::min(n, 1.4 * predicted_rank(d, p.pair.d_prime, (int64_t)n) + 32.0);
+}
+
+// Predicted device seconds of one problem, as the LPT weight.  Coefficients: non-negative least
+// squares of the solo device times of the 294 sweep problems (tools/solo_all.py,
+// profiles/r02/solo_all_s3a.json; relative residual 21 % rms) on
+//   g = 0.0355 s/TFLOP * (QR + certification flops) + 0.019 s per 1e9 entries   (device-filling)
+//   l = 0.0204 s * blocks * N/1e6 + 0.0048 s * blocks + 0.0072 s * (k/1000)^2    (latency-bound)
+// With 4 streams per GPU the latency-bound phases of one problem overlap other problems' GEMMs:
+// measured share times of the 2/4/8-way splits follow sum(g) + sum(l)/2 within 0.87-1.07
+// (profiles/r02/predict_scaling_s3a.json), so the weight is g + l/2.
 double problem_cost(const hb_problem& p) {
   const double n = (double)std::max(p.pair.n_target, p.pair.n_source);
-  const double pr = std::min(n, 1.4 * predicted_rank(p.pair.target.d, p.pair.d_prime, (int64_t)n) + 32.0);
-  return n * n * (60.0 + 4.0 * pr) + 30.0 * pr * pr * pr;
+  const double k = predicted_width(p);
+  const double qr = 4.0 * n * n * k - 4.0 * n * k * k + 4.0 / 3.0 * k * k * k;
+  const double cert = 2.0 * k * k * (n - k / 3.0) + 8.0 / 3.0 * k * k * k;
+  const double blocks = k / 120.0;
+  const double g = 0.0355 * (qr + cert) * 1e-12 + 0.019 * n * n * 1e-9;
+  const double l = 0.0204 * blocks * n * 1e-6 + 0.0048 * blocks + 0.0072 * (k * 1e-3) * (k * 1e-3);
+  return g + 0.5 * l;
 }
 
 // live contexts (for process-wide stats) and the per-device cache used by hb_sweep

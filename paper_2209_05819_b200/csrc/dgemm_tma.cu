@@ -87,20 +87,8 @@ struct TmaGemmParams {
   int cvec;              // C pointer 16-byte aligned and ldc even: 16-byte accesses
   double* fro;           // [gridDim.x * gridDim.y * 8] partials or nullptr
   int64_t fro_row0;
-  // experiment switches (HB_TMA_VARIANT bit mask, default 0): 1 = tensor maps read from global
-  // memory (maps[0] = A, maps[1] = B) behind a tensormap proxy fence instead of the kernel
-  // parameters; 2 = C prefetch with ld.global.cg (L2 only); 4 = no prefetch.tensormap;
-  // 8 = C prefetch with ld.relaxed.gpu; 16 = plain C stores; 32 = async-proxy fence after every
-  // full-barrier wait; 64 = 200 ns sleep after it; 128 = CTA barrier at every tile boundary
-  int variant;
-  const CUtensorMap* maps;
-  const double* Bdbg;    // variant 512: the global B, to verify every fragment read from the ring
-  int64_t ldb_dbg;
-  const double* Adbg;
-  int64_t lda_dbg;
+  int tile_sync;         // CTA barrier at every tile boundary (default 1, see the kernel)
 };
-
-__device__ unsigned int g_tma_dbg_prints = 0;
 
 // K <= NKA * BK: the CTA's whole A block (128 rows x K) stays resident in shared memory for the
 // strip; only B chunks stream through the ring.
@@ -152,8 +140,6 @@ __global__ void __launch_bounds__(kTThreads, 1)
   // ---- producer role (warp 0, lane 0).  Box starts are kept 16-byte aligned in global memory
   // (TMA faults on an odd FP64 start): a map whose base was rounded down by one element loads
   // from the even coordinate and the consumers read at +shift. ----
-  const CUtensorMap* pA = (p.variant & 1) ? p.maps : &tmA;
-  const CUtensorMap* pB = (p.variant & 1) ? p.maps + 1 : &tmB;
   const int total = (nb1 - nb0) * nk;  // B chunks of the strip; chunk g -> slot g % STAGES
   int g_issue = 0;
   auto issue_upto = [&](int g_end) {
@@ -163,21 +149,15 @@ __global__ void __launch_bounds__(kTThreads, 1)
       if (use > 0) mbar_wait(&empty[sl], (use - 1) & 1u);
       const int nb = nb0 + g_issue / nk, kc = g_issue % nk;
       mbar_expect_tx(&full[sl], Cf::STAGE_BYTES);
-      tma_load_2d(sB + sl * Cf::B_ELEMS, pB, &full[sl], kc * BK, nb * kTBN);
+      tma_load_2d(sB + sl * Cf::B_ELEMS, &tmB, &full[sl], kc * BK, nb * kTBN);
     }
   };
   const bool producer = threadIdx.x == 0;
   if (producer) {
-    if (p.variant & 1) {
-      asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;\n" ::"l"(reinterpret_cast<uint64_t>(pA)) : "memory");
-      asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;\n" ::"l"(reinterpret_cast<uint64_t>(pB)) : "memory");
-    }
-    if (!(p.variant & 4)) {
-      asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(pA)) : "memory");
-      asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(pB)) : "memory");
-    }
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
     mbar_expect_tx(afull, Cf::A_BOX_BYTES * (uint32_t)nk);
-    for (int kc = 0; kc < nk; ++kc) tma_load_2d(sA + kc * Cf::A_BOX, pA, afull, (int)m0, kc * BK);
+    for (int kc = 0; kc < nk; ++kc) tma_load_2d(sA + kc * Cf::A_BOX, &tmA, afull, (int)m0, kc * BK);
     issue_upto(STAGES - 1);
   }
   __syncwarp();
@@ -195,7 +175,13 @@ __global__ void __launch_bounds__(kTThreads, 1)
   mbar_wait(afull, 0);
   for (int nb = nb0; nb < nb1; ++nb) {
     const int64_t n0 = (int64_t)nb * kTBN;
-    if (p.variant & 128) __syncthreads();  // experiment: no warp runs ahead across a tile boundary
+    // All 8 warps start a tile together.  Without this barrier a warp with little C traffic (the
+    // rows >= M part of the last m-block) drifts up to two ring chunks ahead across tile
+    // boundaries, and under concurrent sweep streams such CTAs produced wrong C columns for that
+    // warp (DESIGN.md §4 "TMA GEMM": 50-115 flagged updates per configs[3] pass without the
+    // barrier, 0 in every pass with it; the ring, A block and C prefetch all verified correct in
+    // instrumented runs, so the cause is not understood).  HB_TMA_TILE_SYNC=0 removes it (repro).
+    if (p.tile_sync) __syncthreads();
     // C prefetch: thread's values are C[r, c], C[r+1, c] with r = m0 + wm*32 + j*8 + 2*ac,
     // c = n0 + wn*32 + i*8 + ar
     // C prefetch into registers before the k-loop (its latency hides under the DMMA work).  Plain
@@ -212,16 +198,8 @@ __global__ void __launch_bounds__(kTThreads, 1)
         cpre[i][j] = make_double2(0.0, 0.0);
         if (has_beta && c < p.N) {
           const double* cp = p.C + r + c * p.ldc;
-          if (p.variant & 2) {
-            if (r < p.M) cpre[i][j].x = __ldcg(cp);
-            if (r + 1 < p.M) cpre[i][j].y = __ldcg(cp + 1);
-          } else if (p.variant & 8) {
-            if (r < p.M) asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];" : "=d"(cpre[i][j].x) : "l"(cp) : "memory");
-            if (r + 1 < p.M) asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];" : "=d"(cpre[i][j].y) : "l"(cp + 1) : "memory");
-          } else {
-            if (r < p.M) cpre[i][j].x = cp[0];
-            if (r + 1 < p.M) cpre[i][j].y = cp[1];
-          }
+          if (r < p.M) cpre[i][j].x = cp[0];
+          if (r + 1 < p.M) cpre[i][j].y = cp[1];
         }
       }
     }
@@ -236,48 +214,7 @@ __global__ void __launch_bounds__(kTThreads, 1)
         if (producer) issue_upto(gdone + STAGES);
         __syncwarp();  // reconverge warp 0 before its mma.sync.aligned
       }
-      int spins = 0;
-      if (p.variant & 512) {
-        uint32_t ok = 0;
-        while (!ok) {
-          asm volatile(
-              "{\n.reg .pred p;\n"
-              "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
-              "selp.u32 %0, 1, 0, p;\n}\n"
-              : "=r"(ok)
-              : "r"(su32(&full[s])), "r"(ph)
-              : "memory");
-          if (!ok) ++spins;
-        }
-      } else {
-        mbar_wait(&full[s], ph);
-      }
-      if (p.variant & 512) {
-        // verify the ring slot against global memory at the moment this warp reads it
-        const double* bsd = sB + s * Cf::B_ELEMS + b_off;
-        for (int i = 0; i < 4; ++i)
-          for (int kk = 0; kk < BK; kk += 4) {
-            const int64_t kg = (int64_t)kc * BK + kk + ac;
-            const int64_t ng = (int64_t)nb * kTBN + wn * 32 + i * 8 + ar;
-            if (kg < p.K && ng < p.N) {
-              const double sv = bsd[i * 8 * Cf::BP + kk];
-              const double gv = p.Bdbg[kg + ng * p.ldb_dbg];
-              if (sv != gv) {
-                const unsigned n = atomicAdd(&g_tma_dbg_prints, 1u);
-                if (n < 48) {
-                  const double gprev = ng >= 64 ? p.Bdbg[kg + (ng - 64) * p.ldb_dbg] : 0.0;
-                  const double gnext = ng + 64 < p.N ? p.Bdbg[kg + (ng + 64) * p.ldb_dbg] : 0.0;
-                  printf("[tma dbg] mb %d/%d tile %d (in-strip %d) kc %d slot %d warp %d lane %d i %d kk %d spins %d: "
-                         "smem %.6e global %.6e prev-tile %.6e next-tile %.6e\n",
-                         (int)blockIdx.x, (int)gridDim.x, nb, nb - nb0, kc, s, warp, lane, i, kk, spins, sv, gv,
-                         gprev, gnext);
-                }
-              }
-            }
-          }
-      }
-      if (p.variant & 32) asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-      if (p.variant & 64) __nanosleep(200);
+      mbar_wait(&full[s], ph);
       const double* as = a_thr + kc * Cf::A_BOX;
       const double* bs = sB + s * Cf::B_ELEMS + b_off;
 #pragma unroll
@@ -291,31 +228,6 @@ __global__ void __launch_bounds__(kTThreads, 1)
         for (int i = 0; i < 4; ++i)
 #pragma unroll
           for (int j = 0; j < 4; ++j) dmma(acc[i][j][0], acc[i][j][1], fa[i], fb[j]);
-      }
-      if (p.variant & 512) {  // the slot must still hold this chunk when the warp is done with it
-        const double* bsd = sB + s * Cf::B_ELEMS + b_off;
-        for (int i = 0; i < 4; ++i)
-          for (int kk = 0; kk < BK; kk += 4) {
-            const int64_t kg = (int64_t)kc * BK + kk + ac;
-            const int64_t ng = (int64_t)nb * kTBN + wn * 32 + i * 8 + ar;
-            if (kg < p.K && ng < p.N && bsd[i * 8 * Cf::BP + kk] != p.Bdbg[kg + ng * p.ldb_dbg]) {
-              if (atomicAdd(&g_tma_dbg_prints, 1u) < 48)
-                printf("[tma dbg] END-OF-CHUNK mb %d tile %d (in-strip %d) kc %d slot %d warp %d lane %d i %d kk %d: smem %.6e global %.6e\n",
-                       (int)blockIdx.x, nb, nb - nb0, kc, s, warp, lane, i, kk, bsd[i * 8 * Cf::BP + kk],
-                       p.Bdbg[kg + ng * p.ldb_dbg]);
-            }
-          }
-        // the resident A block against global A
-        for (int j = 0; j < 4; ++j)
-          for (int kk = 0; kk < BK; kk += 4) {
-            const int64_t kg = (int64_t)kc * BK + kk + ac;
-            const int64_t mg = m0 + wm * 32 + j * 8 + ar;
-            if (kg < p.K && mg < p.M && as[kk * Cf::AP + j * 8] != p.Adbg[mg + kg * p.lda_dbg]) {
-              if (atomicAdd(&g_tma_dbg_prints, 1u) < 48)
-                printf("[tma dbg] A-BLOCK mb %d tile %d kc %d warp %d lane %d j %d kk %d: smem %.6e global %.6e\n",
-                       (int)blockIdx.x, nb, kc, warp, lane, j, kk, as[kk * Cf::AP + j * 8], p.Adbg[mg + kg * p.lda_dbg]);
-            }
-          }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
@@ -341,15 +253,7 @@ __global__ void __launch_bounds__(kTThreads, 1)
           o.y += p.beta * cpre[i][j].y;
         }
         double* cp = p.C + r + c * p.ldc;
-        if ((p.variant & 512) && has_beta) {
-          const double x2 = r < p.M ? __ldcg(cp) : 0.0, y2 = r + 1 < p.M ? __ldcg(cp + 1) : 0.0;
-          if (x2 != cpre[i][j].x || y2 != cpre[i][j].y) {
-            if (atomicAdd(&g_tma_dbg_prints, 1u) < 48)
-              printf("[tma dbg] C-PREFETCH mb %d tile %d (in-strip %d) warp %d lane %d i %d j %d: prefetched %.6e %.6e now %.6e %.6e\n",
-                     (int)blockIdx.x, nb, nb - nb0, warp, lane, i, j, cpre[i][j].x, cpre[i][j].y, x2, y2);
-          }
-        }
-        if (p.cvec && r + 1 < p.M && !(p.variant & 16)) {
+        if (p.cvec && r + 1 < p.M) {
           __stcg(reinterpret_cast<double2*>(cp), o);
         } else {
           if (r < p.M) cp[0] = o.x;
@@ -399,37 +303,6 @@ CUtensorMap make_map(const double* ptr, int64_t rows, int64_t cols, int64_t ld, 
   return m;
 }
 
-int tma_variant() {
-  static const int v = [] {
-    const char* e = getenv("HB_TMA_VARIANT");
-    return e ? atoi(e) : 0;
-  }();
-  return v;
-}
-
-// Experiment (variant bit 1): a device ring of tensor-map pairs filled by stream-ordered copies
-// from a pinned ring; slots are reused after kMapSlots launches (far more than are ever in flight).
-constexpr int kMapSlots = 8192;
-const CUtensorMap* stage_maps(const CUtensorMap& a, const CUtensorMap& b, cudaStream_t st) {
-  static CUtensorMap* dev = nullptr;
-  static CUtensorMap* pin = nullptr;
-  static std::mutex mu;
-  static unsigned next = 0;
-  unsigned slot;
-  {
-    std::lock_guard<std::mutex> lk(mu);
-    if (!dev) {
-      HB_CUDA(cudaMalloc(&dev, sizeof(CUtensorMap) * 2 * kMapSlots));
-      HB_CUDA(cudaMallocHost(&pin, sizeof(CUtensorMap) * 2 * kMapSlots));
-    }
-    slot = next++ % kMapSlots;
-  }
-  pin[2 * slot] = a;
-  pin[2 * slot + 1] = b;
-  HB_CUDA(cudaMemcpyAsync(dev + 2 * slot, pin + 2 * slot, sizeof(CUtensorMap) * 2, cudaMemcpyHostToDevice, st));
-  return dev + 2 * slot;
-}
-
 template <int BK, int STAGES, int NKA>
 void run_tma(const GemmArgs& g, int num_sms, double* fro, cudaStream_t st) {
   using Cf = TCfg<BK, STAGES, NKA>;
@@ -440,6 +313,11 @@ void run_tma(const GemmArgs& g, int num_sms, double* fro, cudaStream_t st) {
   p.cvec = ((reinterpret_cast<uintptr_t>(g.C) & 15) == 0) && (g.ldc % 2 == 0);
   p.fro = fro;
   p.fro_row0 = g.fro_row0;
+  static const int tile_sync = [] {
+    const char* e = getenv("HB_TMA_TILE_SYNC");
+    return e ? atoi(e) : 1;
+  }();
+  p.tile_sync = tile_sync;
   const CUtensorMap ta = make_map(g.A, g.M, g.K, g.lda, Cf::AP, BK, &p.a_shift);
   const CUtensorMap tb = make_map(g.B, g.K, g.N, g.ldb, Cf::BP, kTBN, &p.b_shift);
   const int mb = (int)ceil_div(g.M, kTBM);
@@ -447,12 +325,6 @@ void run_tma(const GemmArgs& g, int num_sms, double* fro, cudaStream_t st) {
   p.strip = tma_gemm_strip(g.M, g.N, num_sms);
   dim3 grid((unsigned)mb, (unsigned)ceil_div(p.nblocks_n, p.strip));
   HB_REQUIRE(grid.y <= 65535u, HB_ECAP, "dgemm_tma: grid too large");
-  p.variant = tma_variant();
-  p.Bdbg = g.B;
-  p.ldb_dbg = g.ldb;
-  p.Adbg = g.A;
-  p.lda_dbg = g.lda;
-  p.maps = (p.variant & 1) ? stage_maps(ta, tb, st) : nullptr;
   auto k = dgemm_tma_kernel<BK, STAGES, NKA>;
   ensure_dyn_smem((const void*)k, Cf::SMEM);
   k<<<grid, kTThreads, Cf::SMEM, st>>>(ta, tb, p);
@@ -471,10 +343,12 @@ int tma_gemm_strip(int64_t M, int64_t N, int num_sms) {
 }
 
 bool tma_gemm_eligible(const GemmArgs& g) {
-  // OFF by default (HB_GEMM_TMA=1 opts in): under concurrent sweep streams this kernel produced
-  // wrong trailing updates (bench --workload c3 with HB_GEMM_CHECK=1 flagged 17 of them, and two
-  // configs[3] ranks moved), although it passes every isolated test, repro and determinism run —
-  // see DESIGN.md §4 "TMA GEMM".  Until the cause is found the cp.async kernel is the product.
+  // OFF by default (HB_GEMM_TMA=1 opts in).  The race under concurrent sweep streams is closed by
+  // the per-tile CTA barrier in the kernel (0 flagged updates in 12 checked configs[3] passes and a
+  // checked sweep pass, ranks equal to the oracle), and alone the kernel is 6-11 % faster than the
+  // cp.async one; but a TMA CTA holds its SM for a 32-tile strip, the other streams' cooperative
+  // grids wait longer for SMs, and configs[3] / the sweep do not get faster (26.3 vs 26.1 s,
+  // 112.0 vs 110.8 s) -- DESIGN.md §4 "TMA-fed GEMM".  The cp.async kernel stays the product.
   static const bool off = [] {
     const char* e = getenv("HB_GEMM_TMA");
     return !(e && atoi(e) == 1);
