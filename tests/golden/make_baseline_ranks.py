@@ -13,7 +13,7 @@ N = 16000, then the large-N problems by predicted cost).  ``--validate`` first r
 N = 8000 full-SVD records through the certified route (tests/golden/certified_validation.json).
 
 Usage: python tests/golden/make_baseline_ranks.py [max_N] [d:kernel]
-       python tests/golden/make_baseline_ranks.py --certified [--validate] [--max-cost SECONDS]
+       python tests/golden/make_baseline_ranks.py --certified [--validate] [--max-cost SECONDS] [--c3-first]
   (default 4000; 8000 takes ~1 h on 8 cores; "2:log_r" restricts to one dimension and kernel,
   used for the configs[1] N = 16000 entries)
 Runs anywhere the oracle builds (no GPU, no /root/reference needed); results are merged into the
@@ -109,7 +109,11 @@ def main_certified(argv) -> int:
                   f"{c['seconds']}s", flush=True)
             vout.write_text(json.dumps(vals, indent=0) + "\n")
     max_cost = float(argv[argv.index("--max-cost") + 1]) if "--max-cost" in argv else math.inf
-    for key in certified_plan(recs):
+    plan = certified_plan(recs)
+    if "--c3-first" in argv:  # the bench default's own problems (configs[3]) before the rest
+        c3 = [k for k in plan if k[0] == 4 and k[2] == "exp_neg_r"]
+        plan = c3 + [k for k in plan if k not in c3]
+    for key in plan:
         recs = json.loads(OUT.read_text())
         if any((r["d"], r["dprime"], r["kernel"], r["N"]) == key for r in recs):
             continue
