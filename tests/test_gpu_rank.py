@@ -7,6 +7,8 @@
 * Full-size properties where the CPU oracle cannot follow (N up to 65536): certified bracket,
   rank(K) == rank(Kᵀ), monotonicity in the tolerance, determinism.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -342,3 +344,32 @@ def test_fp_band_reported(ctx, hb, oracle):
         want = np.sqrt(n) * 2.0 ** -53 * fro / (tol * r.sigma1)
         assert r.fp_band == pytest.approx(want, rel=1e-9)
         assert r.in_fp_band == (r.gap < r.fp_band)
+
+
+def test_tma_update_gemm_under_concurrent_streams(hb):
+    """The opt-in TMA update GEMM (HB_GEMM_TMA=1) under the concurrent sweep streams that exposed
+    its race: every TMA-routed GEMM is re-run by the cp.async kernel
+    (HB_GEMM_CHECK=1) and must agree, and the ranks must equal the default path's.  Runs in a
+    child process because the routing switches are read once per process."""
+    import json
+    import subprocess
+    import sys
+    from conftest import ROOT
+    spec = [(4, 3, "exp_neg_r", 32000), (4, 2, "exp_neg_r", 32000), (4, 3, "one_over_r", 16000),
+            (4, 1, "exp_neg_r", 32000), (3, 2, "one_over_r", 16000)]
+    probs = [hb.make_problem(k, d, dp, n, [1e-12, 1e-10] if d == 4 else [1e-12]) for (d, dp, k, n) in spec]
+    want, st = hb.sweep(probs, [0])
+    assert st == [0] * len(probs)
+    child = (
+        "import json, sys; sys.path.insert(0, %r); import paper_2209_05819_b200 as hb\n"
+        "spec = %r\n"
+        "probs = [hb.make_problem(k, d, dp, n, [1e-12, 1e-10] if d == 4 else [1e-12]) for (d, dp, k, n) in spec]\n"
+        "res, st = hb.sweep(probs, [0])\n"
+        "print(json.dumps({'st': st, 'ranks': [[x.rank for x in r] for r in res]}))\n" % (str(ROOT), spec))
+    env = dict(os.environ, HB_GEMM_TMA="1", HB_GEMM_CHECK="1")
+    out = subprocess.run([sys.executable, "-c", child], env=env, capture_output=True, text=True, timeout=900)
+    assert out.returncode == 0, out.stderr[-2000:]
+    assert "[gemm check]" not in out.stderr, out.stderr[:2000]
+    got = json.loads(out.stdout.strip().splitlines()[-1])
+    assert got["st"] == [0] * len(probs)
+    assert got["ranks"] == [[x.rank for x in r] for r in want]
