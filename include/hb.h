@@ -333,7 +333,10 @@ hb_status hb_sweep_ex(const hb_problem* probs, int64_t n, const int32_t* devices
 /* Free the per-device contexts cached by hb_sweep / hb_sweep_ex. */
 void hb_sweep_release(void);
 
-/* LPT assignment used by hb_sweep / multi-process sweeps: owner[i] in [0, nparts). */
+/* LPT assignment used by hb_sweep / multi-process sweeps: owner[i] in [0, nparts).  The weight of
+ * a problem is its predicted device time (GEMM-bound part + half of the latency-bound part, from
+ * the predicted factorisation width).  Replaces the reference's parallel_for over
+ * independent blocks (parallel.hpp:12-29) as the unit of distribution.  Host-only, deterministic. */
 hb_status hb_partition(const hb_problem* probs, int64_t n, int32_t nparts, int32_t* owner);
 
 /* ---- ACA: the reference's own rank(ε) factorisation (aca.hpp:16-213) --------------------------

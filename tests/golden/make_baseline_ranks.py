@@ -14,6 +14,8 @@ N = 8000 full-SVD records through the certified route (tests/golden/certified_va
 
 Usage: python tests/golden/make_baseline_ranks.py [max_N] [d:kernel]
        python tests/golden/make_baseline_ranks.py --certified [--validate] [--max-cost SECONDS] [--c3-first]
+              [--skip-c3] [--out FILE] [--deadline SECONDS]
+       python tests/golden/make_baseline_ranks.py --merge FILE
   (default 4000; 8000 takes ~1 h on 8 cores; "2:log_r" restricts to one dimension and kernel,
   used for the configs[1] N = 16000 entries)
 Runs anywhere the oracle builds (no GPU, no /root/reference needed); results are merged into the
@@ -109,29 +111,57 @@ def main_certified(argv) -> int:
                   f"{c['seconds']}s", flush=True)
             vout.write_text(json.dumps(vals, indent=0) + "\n")
     max_cost = float(argv[argv.index("--max-cost") + 1]) if "--max-cost" in argv else math.inf
+    # --out FILE: append the new records to FILE instead of the tracked fixture (a second machine
+    # working on another part of the plan; merge with --merge FILE afterwards)
+    out = Path(argv[argv.index("--out") + 1]) if "--out" in argv else OUT
+    deadline = time.time() + float(argv[argv.index("--deadline") + 1]) if "--deadline" in argv else math.inf
     plan = certified_plan(recs)
+    c3 = [k for k in plan if k[0] == 4 and k[2] == "exp_neg_r"]
     if "--c3-first" in argv:  # the bench default's own problems (configs[3]) before the rest
-        c3 = [k for k in plan if k[0] == 4 and k[2] == "exp_neg_r"]
         plan = c3 + [k for k in plan if k not in c3]
+    if "--skip-c3" in argv:
+        plan = [k for k in plan if k not in c3]
     for key in plan:
         recs = json.loads(OUT.read_text())
-        if any((r["d"], r["dprime"], r["kernel"], r["N"]) == key for r in recs):
+        extra = json.loads(out.read_text()) if out != OUT and out.exists() else []
+        if any((r["d"], r["dprime"], r["kernel"], r["N"]) == key for r in recs + extra):
             continue
         est = 4.0 * key[3] ** 2 * 1.4 * predicted_rank(recs, *key) / 20e9
         if est > max_cost:
             print(f"skip {key}: predicted {est:.0f}s > {max_cost}", flush=True)
             continue
+        if time.time() + 2.0 * est > deadline:
+            print(f"skip {key}: predicted {est:.0f}s would pass the deadline", flush=True)
+            continue
         rec = certified_record(*key, nthreads)
-        recs = json.loads(OUT.read_text())
-        recs.append(rec)
-        OUT.write_text(json.dumps(recs, indent=0) + "\n")
+        if out == OUT:
+            recs = json.loads(OUT.read_text())
+            recs.append(rec)
+            OUT.write_text(json.dumps(recs, indent=0) + "\n")
+        else:
+            extra = json.loads(out.read_text()) if out.exists() else []
+            extra.append(rec)
+            out.write_text(json.dumps(extra, indent=0) + "\n")
         print(f"{key}: ranks {rec['ranks']} [{rec['rank_lo']}, {rec['rank_hi']}] k={rec['k']} "
               f"gaps {[f'{g:.1e}' for g in rec['gaps']]} {rec['seconds']}s {rec['phase_s']}",
               flush=True)
     return 0
 
 
+def main_merge(path) -> int:
+    """Merge records produced elsewhere with --out into the tracked fixture (no duplicates)."""
+    recs = json.loads(OUT.read_text())
+    have = {(r["d"], r["dprime"], r["kernel"], r["N"]) for r in recs}
+    new = [r for r in json.loads(Path(path).read_text())
+           if (r["d"], r["dprime"], r["kernel"], r["N"]) not in have]
+    OUT.write_text(json.dumps(recs + new, indent=0) + "\n")
+    print(f"merged {len(new)} records -> {len(recs) + len(new)}")
+    return 0
+
+
 def main() -> int:
+    if "--merge" in sys.argv:
+        return main_merge(sys.argv[sys.argv.index("--merge") + 1])
     if "--certified" in sys.argv:
         return main_certified(sys.argv)
     max_n = int(sys.argv[1]) if len(sys.argv) > 1 else 4000

@@ -318,7 +318,9 @@ def test_sweep_two_workers_one_device_matches_single(ctx, hb):
     for a, b in zip(one, two):
         assert [x.rank for x in a] == [x.rank for x in b]
         assert [x.k_factored for x in a] == [x.k_factored for x in b]
-        assert [x.sigma1 for x in a] == [x.sigma1 for x in b]
+        # a problem may land on a stream with another SM share: its cooperative reductions then sum
+        # a different number of partials, so sigma can differ in the last bits (never the counts)
+        assert [x.sigma1 for x in a] == pytest.approx([x.sigma1 for x in b], rel=1e-12)
 
 
 def test_sweep_bad_arguments_reported(hb):
