@@ -197,10 +197,6 @@ __global__ void __launch_bounds__(Cfg<TA, WARPS_M, WARPS_N, WM, WN, BK_, ST_>::N
     cp_commit();
   }
   const int ar = lane >> 2, ac = lane & 3;
-  // M tail: 8-row fragments of this warp that lie entirely at or beyond row M are skipped (the
-  // skinny W = V^T A2 reduce has M = b = 120 in a 128-row tile: 1 of 16 fragments, 6 % of its DMMAs)
-  const int64_t wrow0 = m0 + (int64_t)wm * WM * 8;
-  const int wm_valid = wrow0 >= p.M ? 0 : (int)min((int64_t)WM, (p.M - wrow0 + 7) / 8);
   for (int kt = 0; kt < nk; ++kt) {
     cp_wait<STAGES - 2>();
     __syncthreads();
@@ -211,12 +207,8 @@ __global__ void __launch_bounds__(Cfg<TA, WARPS_M, WARPS_N, WM, WN, BK_, ST_>::N
     }
     const double* as = As + (kt % STAGES) * C_::A_ELEMS;
     const double* bs = Bs + (kt % STAGES) * C_::B_ELEMS;
-    // K tail: the last k-tile only runs its valid k-steps (the rest of the tile is zero-filled;
-    // at K = 120, BK = 32 that is 2 of 32 k-steps, 6 % of the DMMA work of the rank-b update)
-    const int kk_end = kt + 1 < nk ? BK : (int)(((kend - kbeg - (int64_t)kt * BK) + 3) & ~(int64_t)3);
-#pragma unroll
-    for (int kk = 0; kk < BK; kk += 4) {
-      if (kk >= kk_end) break;
+    // one k-step (4 deep) of the warp tile
+    auto kstep = [&](int kk) {
       double a[WM], b[WN];
 #pragma unroll
       for (int i = 0; i < WM; ++i) {
@@ -229,11 +221,21 @@ __global__ void __launch_bounds__(Cfg<TA, WARPS_M, WARPS_N, WM, WN, BK_, ST_>::N
         b[j] = bs[n * (BK + 4) + kk + ac];
       }
 #pragma unroll
-      for (int i = 0; i < WM; ++i) {
-        if (i >= wm_valid) break;
+      for (int i = 0; i < WM; ++i)
 #pragma unroll
         for (int j = 0; j < WN; ++j) dmma884(acc[i][j][0], acc[i][j][1], a[i], b[j]);
-      }
+    };
+    const int64_t krem = kend - kbeg - (int64_t)kt * BK;
+    if (krem >= BK) {
+#pragma unroll
+      for (int kk = 0; kk < BK; kk += 4) kstep(kk);
+    } else {
+      // K tail: the last k-tile runs only its valid k-steps (the rest of the tile is zero-filled;
+      // at K = b = 120, BK = 32 that saves 2 of the update's 32 k-steps), in a rolled loop so the
+      // unrolled body above stays as it was
+      const int kk_end = (int)((krem + 3) & ~(int64_t)3);
+#pragma unroll 1
+      for (int kk = 0; kk < kk_end; kk += 4) kstep(kk);
     }
   }
   cp_wait<0>();

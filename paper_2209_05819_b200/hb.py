@@ -162,7 +162,8 @@ def load(path: os.PathLike | str | None = None):
     global _lib
     if _lib is not None and path is None:
         return _lib
-    p = Path(path) if path else LIB_PATH
+    # HB200_LIB: another build of the library (A/B comparisons of kernels; tools only)
+    p = Path(path) if path else Path(os.environ.get("HB200_LIB", LIB_PATH))
     if not p.exists():
         raise FileNotFoundError(f"{p} is missing: run `make -C paper_2209_05819_b200` "
                                 f"(or __graft_entry__.build())")
