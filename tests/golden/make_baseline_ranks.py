@@ -130,7 +130,7 @@ def main_certified(argv) -> int:
         if est > max_cost:
             print(f"skip {key}: predicted {est:.0f}s > {max_cost}", flush=True)
             continue
-        if time.time() + 2.0 * est > deadline:
+        if time.time() + 1.3 * est > deadline:
             print(f"skip {key}: predicted {est:.0f}s would pass the deadline", flush=True)
             continue
         rec = certified_record(*key, nthreads)
